@@ -1,0 +1,121 @@
+/*
+ * rdfft.h — C-ABI of librdfft.so: the B200 (sm_100a) hot path of rdFFT,
+ * "in-place real-domain FFT" (arXiv 2511.01385).
+ *
+ * Citations: P:Lxxx = PAPER.md line; readings C1..C16 are listed in DESIGN.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Pointers x, a, b, w, y, g, dx, dw are DEVICE pointers (cudaMalloc / torch
+ *    CUDA tensors).  Buffers are row-major with contiguous rows: a batch of
+ *    vectors is [batch][n]; BCA activations are [T][d] with each row made of
+ *    d/p consecutive length-p blocks (reading C14).
+ *  - dtype is RDFFT_F32 (IEEE fp32) or RDFFT_BF16 (bfloat16 storage).  All
+ *    arithmetic is fp32 in registers; bf16 results are rounded to nearest even
+ *    on store (reading C7).  dw is always fp32.
+ *  - n (the transform length, or the BCA block size p) is a power of two with
+ *    2 <= n <= 4096 (reading C9).
+ *  - stream is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    asynchronous on that stream; inputs are validated synchronously on the
+ *    host before anything is launched, and nothing is launched on error.
+ *  - Ownership: the caller owns every buffer.  The library allocates NO device
+ *    or host memory per call (no scratch, no plan object, no hidden state);
+ *    twiddle factors are generated on chip.  One buffer must not be used by
+ *    two concurrent calls.
+ *  - Base pointers must be 16-byte aligned (torch allocations are 256 B); the
+ *    kernels use 128-bit accesses.  Any batch, including ragged tails, is
+ *    handled.
+ *  - batch == 0 (or T == 0) is a successful no-op.
+ *  - Non-finite inputs are not checked; IEEE propagation applies.
+ *  - Return value: rdfft_status_t.  RDFFT_E_CUDA reports a launch error
+ *    (cudaGetLastError after launch); asynchronous faults surface on the
+ *    stream as usual.
+ *
+ * Packed layout ("Squeeze N+2 into N" / "Memory Layout Design"):
+ *    slot 0 = Re y_0,  slot n/2 = Re y_{n/2},
+ *    slot k = Re y_k,  slot n-k = Im y_k   for 1 <= k < n/2   (reading C2),
+ *  with y_k = sum_t x_t exp(-2 pi i k t / n)  (Eq. 1; reading C3).
+ */
+#ifndef RDFFT_H
+#define RDFFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { RDFFT_F32 = 0, RDFFT_BF16 = 1 } rdfft_dtype_t;
+
+typedef enum {
+  RDFFT_OK = 0,
+  RDFFT_E_SIZE = 1,  /* n (or p) not a power of two in [2, 4096]                 */
+  RDFFT_E_NULL = 2,  /* null pointer with a non-empty batch                       */
+  RDFFT_E_ALIGN = 3, /* a base pointer is not 16-byte aligned                     */
+  RDFFT_E_DTYPE = 4, /* dtype not RDFFT_F32 / RDFFT_BF16                          */
+  RDFFT_E_SHAPE = 5, /* negative batch, b_batch not in {1, batch}, d % p != 0     */
+  RDFFT_E_ALIAS = 6, /* forbidden overlap between buffers (see each call)         */
+  RDFFT_E_CUDA = 7   /* the kernel launch failed                                  */
+} rdfft_status_t;
+
+/* rdfft_fwd — batched in-place forward rdFFT (§4.1, Prop. 1).
+ *   x: [batch][n] real signals of `dtype`, overwritten by their packed spectra.
+ *   Equals pack(DFT(x)) row by row; touches no memory outside x.            */
+int rdfft_fwd(void* x, int64_t batch, int64_t n, int dtype, void* stream);
+
+/* rdfft_inv — batched in-place inverse rdFFT (§4.2, Eq. 7).
+ *   x: [batch][n] packed spectra, overwritten by the real signals
+ *   x_t = (1/n) sum_k y_k exp(+2 pi i k t / n)  (1/n included, reading C4). */
+int rdfft_inv(void* x, int64_t batch, int64_t n, int dtype, void* stream);
+
+/* rdfft_packed_mul — a <- a (.) b per frequency bin, in the packed domain
+ * (the product of Hermitian spectra stays Hermitian).
+ *   a: [batch][n] packed spectra (in/out); b: [b_batch][n] packed spectra,
+ *   read only, b_batch == 1 broadcasts b to every row of a.
+ *   b may not overlap a unless b == a and b_batch == batch (RDFFT_E_ALIAS).  */
+int rdfft_packed_mul(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, int dtype,
+                     void* stream);
+
+/* rdfft_packed_conjmul — a <- a (.) conj(b) per bin (Eq. 5 products).
+ *   Same arguments and rules as rdfft_packed_mul.                            */
+int rdfft_packed_conjmul(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, int dtype,
+                         void* stream);
+
+/* bca_fwd — fused block-circulant adapter forward (Eq. 4).
+ *   x: [T][d_in] (read only, NOT modified: reading C13)
+ *   w: [q_out][q_in][p] time-domain first columns c_ij (reading C10, C12),
+ *      q_in = d_in/p, q_out = d_out/p, same dtype as x
+ *   y: [T][d_out] output, y_i = sum_j circ(w_ij) x_j = IrdFFT(sum_j W_ij (.) X_j)
+ *   y may not overlap x or w (RDFFT_E_ALIAS).  d_in % p, d_out % p must be 0. */
+int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
+            int dtype, void* stream);
+
+/* bca_bwd — fused block-circulant adapter backward (Eq. 5, P:L174-183;
+ * blockwise pairing reading C11).  With G_i = rdFFT(g_i), X_j = rdFFT(x_j),
+ * W_ij = rdFFT(w_ij):
+ *   dx_j  = IrdFFT( sum_i conj(W_ij) (.) G_i )              -> dx [T][d_in]
+ *   dw_ij = IrdFFT( sum_t conj(X_tj) (.) G_ti )             -> dw [q_out][q_in][p] fp32
+ *   x, w, g: as in bca_fwd (g = dL/dy, [T][d_out]).
+ *   dx may alias g exactly when d_in == d_out ("overwriting the grad_output
+ *   in-place"); any other overlap of dx with x, w, g is RDFFT_E_ALIAS.
+ *   dw (fp32, 16-byte aligned) is OVERWRITTEN (zeroed on the stream, then
+ *   accumulated); it must not overlap anything.  Accumulation over tokens uses
+ *   fp32 atomics, so dw is reproducible only to rounding, not bitwise.      */
+int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
+            int64_t d_out, int64_t p, int dtype, void* stream);
+
+/* Static, never-allocating description of a status code. */
+const char* rdfft_status_str(int status);
+
+/* Number of kernels this library has launched since load (process-wide,
+ * monotonically increasing).  Used by bench.py to count its GPU launches.   */
+uint64_t rdfft_launch_count(void);
+
+/* Library ABI version (major*100 + minor). */
+int rdfft_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RDFFT_H */

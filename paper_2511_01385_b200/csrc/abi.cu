@@ -1,0 +1,235 @@
+// abi.cu — the C-ABI of librdfft.so (declared and documented in include/rdfft.h).
+//
+// Host side only: validate arguments, pick a kernel configuration from
+// (n, dtype) alone (never from batch, so any sharding of the batch gives
+// bit-identical rows), launch on the caller's stream.  No allocation.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/rdfft.h"
+#include "bca_v1.cuh"
+#include "kernels_v1.cuh"
+#include "rdfft_kernels.cuh"
+
+using namespace rdfft;
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+int ilog2(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+bool pow2_in_range(int64_t n) { return n >= 2 && n <= kMaxN && (n & (n - 1)) == 0; }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const char* pa = static_cast<const char*>(a);
+  const char* pb = static_cast<const char*>(b);
+  return na && nb && pa < pb + nb && pb < pa + na;
+}
+size_t dsize(int dtype) { return dtype == RDFFT_BF16 ? 2 : 4; }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+int launched(int count = 1) {
+  g_launches.fetch_add(count, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess ? RDFFT_OK : RDFFT_E_CUDA;
+}
+
+template <typename T>
+int launch_transform(T* x, int64_t batch, int n, bool inverse, cudaStream_t st) {
+  const int logn = ilog2(n);
+  if (launch_rdfft_fast<T>(x, batch, n, logn, inverse, num_sms(), st)) return launched();
+  const int V = kV1TileElems >> logn;
+  const int64_t tiles = (batch + V - 1) / V;
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 8);
+  if (inverse)
+    rdfft_v1_kernel<T, true><<<grid, kV1Threads, 0, st>>>(x, batch, n, logn);
+  else
+    rdfft_v1_kernel<T, false><<<grid, kV1Threads, 0, st>>>(x, batch, n, logn);
+  return launched();
+}
+
+int transform(void* x, int64_t batch, int64_t n, int dtype, void* stream, bool inverse) {
+  if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return RDFFT_E_DTYPE;
+  if (!pow2_in_range(n)) return RDFFT_E_SIZE;
+  if (batch < 0) return RDFFT_E_SHAPE;
+  if (batch == 0) return RDFFT_OK;
+  if (!x) return RDFFT_E_NULL;
+  if (!aligned16(x)) return RDFFT_E_ALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == RDFFT_F32) return launch_transform<float>(static_cast<float*>(x), batch, (int)n, inverse, st);
+  return launch_transform<__nv_bfloat16>(static_cast<__nv_bfloat16*>(x), batch, (int)n, inverse, st);
+}
+
+int packed(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, int dtype, void* stream, bool conj) {
+  if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return RDFFT_E_DTYPE;
+  if (!pow2_in_range(n)) return RDFFT_E_SIZE;
+  if (batch < 0 || b_batch < 0) return RDFFT_E_SHAPE;
+  if (batch == 0) return RDFFT_OK;
+  if (b_batch != 1 && b_batch != batch) return RDFFT_E_SHAPE;
+  if (!a || !b) return RDFFT_E_NULL;
+  if (!aligned16(a) || !aligned16(b)) return RDFFT_E_ALIGN;
+  const size_t s = dsize(dtype);
+  if (overlap(a, batch * n * s, b, b_batch * n * s) && !(a == b && b_batch == batch)) return RDFFT_E_ALIAS;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int logn = ilog2(n);
+  const int64_t items = batch * (n / 2);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)num_sms() * 16));
+#define RDFFT_PM(T, C) \
+  packed_mul_kernel<T, C><<<grid, 256, 0, st>>>(static_cast<T*>(a), static_cast<const T*>(b), batch, (int)n, logn, b_batch)
+  if (dtype == RDFFT_F32) {
+    if (conj) RDFFT_PM(float, true); else RDFFT_PM(float, false);
+  } else {
+    if (conj) RDFFT_PM(__nv_bfloat16, true); else RDFFT_PM(__nv_bfloat16, false);
+  }
+#undef RDFFT_PM
+  return launched();
+}
+
+int bca_check(const void* x, const void* w, int64_t T, int64_t d_in, int64_t d_out, int64_t p, int dtype) {
+  if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return RDFFT_E_DTYPE;
+  if (!pow2_in_range(p)) return RDFFT_E_SIZE;
+  if (T < 0 || d_in <= 0 || d_out <= 0 || d_in % p || d_out % p) return RDFFT_E_SHAPE;
+  if (!x || !w) return T == 0 ? RDFFT_OK : RDFFT_E_NULL;
+  if (!aligned16(x) || !aligned16(w)) return RDFFT_E_ALIGN;
+  return RDFFT_OK;
+}
+
+template <typename K>
+int grid_for(K kernel, int threads, size_t smem, int64_t units) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm <= 0) return 0;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * num_sms()));
+}
+
+}  // namespace
+
+extern "C" {
+
+int rdfft_fwd(void* x, int64_t batch, int64_t n, int dtype, void* stream) {
+  return transform(x, batch, n, dtype, stream, false);
+}
+
+int rdfft_inv(void* x, int64_t batch, int64_t n, int dtype, void* stream) {
+  return transform(x, batch, n, dtype, stream, true);
+}
+
+int rdfft_packed_mul(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, int dtype, void* stream) {
+  return packed(a, b, batch, n, b_batch, dtype, stream, false);
+}
+
+int rdfft_packed_conjmul(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, int dtype,
+                         void* stream) {
+  return packed(a, b, batch, n, b_batch, dtype, stream, true);
+}
+
+int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p, int dtype,
+            void* stream) {
+  int rc = bca_check(x, w, T, d_in, d_out, p, dtype);
+  if (rc != RDFFT_OK || T == 0) return rc;
+  if (!y) return RDFFT_E_NULL;
+  if (!aligned16(y)) return RDFFT_E_ALIGN;
+  const size_t s = dsize(dtype);
+  const int q_in = (int)(d_in / p), q_out = (int)(d_out / p);
+  if (overlap(y, T * d_out * s, x, T * d_in * s) || overlap(y, T * d_out * s, w, (size_t)q_out * q_in * p * s))
+    return RDFFT_E_ALIAS;
+  const size_t smem = bca_fwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
+  if (smem > 227 * 1024) return RDFFT_E_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int logp = ilog2(p);
+  if (dtype == RDFFT_F32) {
+    auto k = bca_fwd_v1_kernel<float>;
+    const int grid = grid_for(k, kBcaThreads, smem, T);
+    if (!grid) return RDFFT_E_SHAPE;
+    k<<<grid, kBcaThreads, smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
+                                       static_cast<float*>(y), T, q_in, q_out, (int)p, logp);
+  } else {
+    auto k = bca_fwd_v1_kernel<__nv_bfloat16>;
+    const int grid = grid_for(k, kBcaThreads, smem, T);
+    if (!grid) return RDFFT_E_SHAPE;
+    k<<<grid, kBcaThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+                                       static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, logp);
+  }
+  return launched();
+}
+
+int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in, int64_t d_out,
+            int64_t p, int dtype, void* stream) {
+  int rc = bca_check(x, w, T, d_in, d_out, p, dtype);
+  if (rc != RDFFT_OK) return rc;
+  if (!dw) return RDFFT_E_NULL;
+  if (!aligned16(dw)) return RDFFT_E_ALIGN;
+  const size_t s = dsize(dtype);
+  const int q_in = (int)(d_in / p), q_out = (int)(d_out / p);
+  const size_t nw = (size_t)q_out * q_in * p;
+  const size_t xb = T * d_in * s, gb = T * d_out * s;
+  if (T > 0) {
+    if (!g || !dx) return RDFFT_E_NULL;
+    if (!aligned16(g) || !aligned16(dx)) return RDFFT_E_ALIGN;
+    if (overlap(dx, xb, x, xb) || overlap(dx, xb, w, nw * s)) return RDFFT_E_ALIAS;
+    if (overlap(dx, xb, g, gb) && !(dx == g && d_in == d_out)) return RDFFT_E_ALIAS;
+  }
+  if (overlap(dw, nw * 4, x, xb) || overlap(dw, nw * 4, w, nw * s) || overlap(dw, nw * 4, g, gb) ||
+      overlap(dw, nw * 4, dx, xb))
+    return RDFFT_E_ALIAS;
+  const size_t smem = bca_bwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
+  if (smem > 227 * 1024) return RDFFT_E_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(dw, 0, nw * sizeof(float), st) != cudaSuccess) return RDFFT_E_CUDA;
+  const int logp = ilog2(p);
+  if (T > 0) {
+    if (dtype == RDFFT_F32) {
+      auto k = bca_bwd_v1_kernel<float>;
+      const int grid = grid_for(k, kBcaThreads, smem, T);
+      if (!grid) return RDFFT_E_SHAPE;
+      k<<<grid, kBcaThreads, smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
+                                         static_cast<const float*>(g), static_cast<float*>(dx), dw, T, q_in, q_out,
+                                         (int)p, logp);
+    } else {
+      auto k = bca_bwd_v1_kernel<__nv_bfloat16>;
+      const int grid = grid_for(k, kBcaThreads, smem, T);
+      if (!grid) return RDFFT_E_SHAPE;
+      k<<<grid, kBcaThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x),
+                                         static_cast<const __nv_bfloat16*>(w), static_cast<const __nv_bfloat16*>(g),
+                                         static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out, (int)p, logp);
+    }
+    if ((rc = launched()) != RDFFT_OK) return rc;
+  }
+  // dw finalise: in-place inverse rdFFT of the q_out*q_in accumulated fp32 spectra.
+  return launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/true, st);
+}
+
+const char* rdfft_status_str(int status) {
+  switch (status) {
+    case RDFFT_OK: return "ok";
+    case RDFFT_E_SIZE: return "n (or p) is not a power of two in [2, 4096]";
+    case RDFFT_E_NULL: return "null pointer";
+    case RDFFT_E_ALIGN: return "pointer not 16-byte aligned";
+    case RDFFT_E_DTYPE: return "unsupported dtype";
+    case RDFFT_E_SHAPE: return "invalid shape";
+    case RDFFT_E_ALIAS: return "forbidden buffer overlap";
+    case RDFFT_E_CUDA: return "CUDA launch error";
+    default: return "unknown status";
+  }
+}
+
+uint64_t rdfft_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int rdfft_abi_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,82 @@
+// common.cuh — shared device helpers for the rdFFT kernels (sm_100a).
+//
+// Packed layout: slot k = Re y_k, slot n-k = Im y_k (1 <= k < n/2),
+// slot 0 = y_0, slot n/2 = y_{n/2}.  Twiddles W_{2m}^k = exp(-2 pi i k / 2m)
+// (reading C1 of the garbled P:L156) are generated on chip; no global tables.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rdfft {
+
+constexpr int kMaxN = 4096;
+constexpr int kMaxLogN = 12;
+
+// ------------------------------------------------------------ dtype traits
+template <typename T>
+struct io;
+
+template <>
+struct io<float> {
+  static constexpr int kVec = 4;  // elements per 16-byte access
+  __device__ __forceinline__ static float ld(const float* p) { return *p; }
+  __device__ __forceinline__ static void st(float* p, float v) { *p = v; }
+  __device__ __forceinline__ static void unpack16(const uint4& u, float* f) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+  }
+  __device__ __forceinline__ static uint4 pack16(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+};
+
+template <>
+struct io<__nv_bfloat16> {
+  static constexpr int kVec = 8;
+  __device__ __forceinline__ static float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+  __device__ __forceinline__ static void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+  // bf16 -> fp32 is exact: the bf16 bits are the high half of the fp32 word.
+  __device__ __forceinline__ static void unpack16(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  __device__ __forceinline__ static uint32_t pack2(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // RNE (reading C7)
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __device__ __forceinline__ static uint4 pack16(const float* f) {
+    return make_uint4(pack2(f[0], f[1]), pack2(f[2], f[3]), pack2(f[4], f[5]), pack2(f[6], f[7]));
+  }
+};
+
+__device__ __forceinline__ int bitrev(int i, int logn) {
+  return logn == 0 ? 0 : (int)(__brev((unsigned)i) >> (32 - logn));
+}
+
+// tw[j] = W_n^j = (cos 2 pi j/n, -sin 2 pi j/n) for 0 <= j < n/2.  2j/n is exact in fp32.
+__device__ __forceinline__ void make_twiddles(float2* tw, int n) {
+  for (int j = threadIdx.x; j < n / 2; j += blockDim.x) {
+    float s, c;
+    sincospif(2.0f * (float)j / (float)n, &s, &c);
+    tw[j] = make_float2(c, -s);
+  }
+}
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+
+}  // namespace rdfft

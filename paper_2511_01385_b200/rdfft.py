@@ -1,0 +1,168 @@
+"""Thin Python binding of librdfft.so (include/rdfft.h): argument marshalling only.
+
+Every function takes CUDA torch tensors, passes their device pointers, sizes,
+dtype code and torch's current stream to the C-ABI entry point of the same
+name, and raises RdfftError on a non-zero status.  No arithmetic happens
+here; there is no CPU fallback: if the library is missing, import fails.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librdfft.so")
+
+F32, BF16 = 0, 1
+_DT = {torch.float32: F32, torch.bfloat16: BF16}
+
+
+class RdfftError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        self.status = status
+        super().__init__(f"{fn}: status {status}: {_lib().rdfft_status_str(status).decode()}")
+
+
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"librdfft.so not built at {LIB_PATH}; run `python -m paper_2511_01385_b200.build` "
+                "or __graft_entry__.build() (there is no CPU fallback)")
+        lib = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        lib.rdfft_fwd.argtypes = [vp, i64, i64, i32, vp]
+        lib.rdfft_inv.argtypes = [vp, i64, i64, i32, vp]
+        lib.rdfft_packed_mul.argtypes = [vp, vp, i64, i64, i64, i32, vp]
+        lib.rdfft_packed_conjmul.argtypes = [vp, vp, i64, i64, i64, i32, vp]
+        lib.bca_fwd.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
+        lib.bca_bwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
+        for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
+                  "rdfft_abi_version"):
+            getattr(lib, f).restype = i32
+        lib.rdfft_status_str.argtypes = [i32]
+        lib.rdfft_status_str.restype = ctypes.c_char_p
+        lib.rdfft_launch_count.restype = ctypes.c_uint64
+        _LIB = lib
+    return _LIB
+
+
+EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
+           "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(t):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _dtype(t):
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {t.dtype}; rdFFT takes float32 or bfloat16") from None
+
+
+def _check(t, name):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _call(fn, *args):
+    rc = getattr(_lib(), fn)(*args)
+    if rc != 0:
+        raise RdfftError(fn, rc)
+
+
+def rdfft_fwd(x: torch.Tensor) -> torch.Tensor:
+    """In place: rows of x (last dim n) become their packed spectra.  Returns x."""
+    _check(x, "x")
+    n = x.shape[-1]
+    _call("rdfft_fwd", _ptr(x), x.numel() // max(n, 1), n, _dtype(x), _stream(x))
+    return x
+
+
+def rdfft_inv(x: torch.Tensor) -> torch.Tensor:
+    """In place: packed spectra rows of x become real signals (1/n included).  Returns x."""
+    _check(x, "x")
+    n = x.shape[-1]
+    _call("rdfft_inv", _ptr(x), x.numel() // max(n, 1), n, _dtype(x), _stream(x))
+    return x
+
+
+def _packed(fn, a, b):
+    _check(a, "a")
+    _check(b, "b")
+    if b.dtype != a.dtype or b.shape[-1] != a.shape[-1]:
+        raise ValueError("a and b must share dtype and last dimension")
+    n = a.shape[-1]
+    _call(fn, _ptr(a), _ptr(b), a.numel() // n, n, b.numel() // n, _dtype(a), _stream(a))
+    return a
+
+
+def rdfft_packed_mul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """In place a <- a (.) b per bin (b: one row, broadcast, or as many rows as a)."""
+    return _packed("rdfft_packed_mul", a, b)
+
+
+def rdfft_packed_conjmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """In place a <- a (.) conj(b) per bin."""
+    return _packed("rdfft_packed_conjmul", a, b)
+
+
+def bca_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
+    """y = BCA(x) for x [..., d_in], w [q_out, q_in, p]; y [..., q_out*p] (allocated if None)."""
+    _check(x, "x")
+    _check(w, "w")
+    q_out, q_in, p = w.shape
+    d_in, d_out = q_in * p, q_out * p
+    if x.shape[-1] != d_in:
+        raise ValueError(f"x last dim {x.shape[-1]} != q_in*p = {d_in}")
+    if y is None:
+        y = torch.empty(x.shape[:-1] + (d_out,), dtype=x.dtype, device=x.device)
+    _check(y, "y")
+    if w.dtype != x.dtype or y.dtype != x.dtype:
+        raise ValueError("x, w, y must share a dtype")
+    _call("bca_fwd", _ptr(x), _ptr(w), _ptr(y), x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
+    return y
+
+
+def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor | None = None,
+            dw: torch.Tensor | None = None):
+    """(dx, dw) of the BCA layer for dL/dy = g.  dx may be g itself when d_in == d_out
+    (grad_output overwritten in place).  dw is fp32 [q_out, q_in, p]."""
+    _check(x, "x")
+    _check(w, "w")
+    _check(g, "g")
+    q_out, q_in, p = w.shape
+    d_in, d_out = q_in * p, q_out * p
+    if dx is None:
+        dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
+    if dw is None:
+        dw = torch.empty((q_out, q_in, p), dtype=torch.float32, device=x.device)
+    _check(dx, "dx")
+    _check(dw, "dw")
+    if dw.dtype != torch.float32:
+        raise ValueError("dw must be float32 (P:L486)")
+    _call("bca_bwd", _ptr(x), _ptr(w), _ptr(g), _ptr(dx), _ptr(dw), x.numel() // d_in, d_in, d_out, p,
+          _dtype(x), _stream(x))
+    return dx, dw
+
+
+def launch_count() -> int:
+    return int(_lib().rdfft_launch_count())
+
+
+def abi_version() -> int:
+    return int(_lib().rdfft_abi_version())

@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the float64 oracle.
+
+Gates (BASELINE.json north_star): fp32 per-vector rel-L2 <= 1e-5, bf16 (given
+bf16-rounded inputs) <= 2e-2, packed index placement bit-exact.  The oracle
+consumes exactly the values the kernel consumed (bf16 widened exactly to
+float64) and kernel outputs are widened exactly to float64 (reading O8).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as o
+from paper_2511_01385_b200 import rdfft as R
+from paper_2511_01385_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-5, "bf16": 2e-2}
+NS = [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built(cuda_device):
+    from paper_2511_01385_b200 import build
+
+    build.build()
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def rel_l2_rows(out, ref):
+    num = np.linalg.norm(out - ref, axis=-1)
+    den = np.maximum(np.linalg.norm(ref, axis=-1), 1e-300)
+    return (num / den).max()
+
+
+def batch_for(n):
+    # several tiles of every kernel configuration plus a ragged tail
+    return max(3, (1 << 16) // n) * 3 + 5
+
+
+# ------------------------------------------------------------- transforms
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_forward_matches_oracle(n, dtype):
+    b = batch_for(n)
+    x = synth.randn((b, n), seed=100 + n, dtype=dtype).cuda()
+    xin = f64(x)
+    R.rdfft_fwd(x)
+    torch.cuda.synchronize()
+    idx = np.unique(np.r_[0, 1, b - 1, b - 2, np.random.default_rng(n).integers(0, b, 64)])
+    err = rel_l2_rows(f64(x)[idx], o.rdfft_fwd(xin[idx]))
+    assert err <= TOL[dtype], err
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_inverse_matches_oracle(n, dtype):
+    b = batch_for(n)
+    p = synth.randn((b, n), seed=200 + n, dtype=dtype).cuda()
+    pin = f64(p)
+    R.rdfft_inv(p)
+    torch.cuda.synchronize()
+    idx = np.unique(np.r_[0, b - 1, np.random.default_rng(n).integers(0, b, 64)])
+    err = rel_l2_rows(f64(p)[idx], o.rdfft_inv(pin[idx]))
+    assert err <= TOL[dtype], err
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_round_trip(n, dtype):
+    b = batch_for(n)
+    x = synth.randn((b, n), seed=300 + n, dtype=dtype).cuda()
+    x0 = x.clone()
+    R.rdfft_inv(R.rdfft_fwd(x))
+    torch.cuda.synchronize()
+    err = rel_l2_rows(f64(x), f64(x0))
+    assert err <= (1e-5 if dtype == "f32" else 2e-2), err
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", NS)
+def test_layout_probes_bit_exact(n, dtype):
+    """Index placement: impulse -> exact ones in slots 0..n/2;
+    cos at k0 -> slot k0 is the unique large entry (+n/2); sin at k0 -> slot n-k0 (-n/2)."""
+    dt = synth.DTYPES[dtype]
+    t = torch.arange(n, dtype=torch.float64)
+    rows = [torch.zeros(n, dtype=torch.float64)]
+    rows[0][0] = 1
+    ks = list(range(1, n // 2))
+    rows += [torch.cos(2 * np.pi * k * t / n) for k in ks]
+    rows += [torch.sin(2 * np.pi * k * t / n) for k in ks]
+    x = torch.stack(rows).to(dt).cuda()
+    R.rdfft_fwd(x)
+    y = f64(x)
+    want = np.zeros(n)
+    want[: n // 2 + 1] = 1
+    np.testing.assert_array_equal(y[0], want)
+    for r, k in enumerate(ks):
+        c, s = y[1 + r], y[1 + len(ks) + r]
+        assert np.argmax(np.abs(c)) == k and abs(c[k] - n / 2) < 0.05 * n
+        assert np.argmax(np.abs(s)) == n - k and abs(s[n - k] + n / 2) < 0.05 * n
+    # inverse probes: e0 -> 1/n exactly; e_{n/2} -> (-1)^t / n exactly
+    e = torch.zeros(2, n, dtype=dt)
+    e[0, 0] = 1
+    e[1, n // 2] = 1
+    e = e.cuda()
+    R.rdfft_inv(e)
+    z = f64(e)
+    np.testing.assert_array_equal(z[0], np.full(n, 1.0 / n))
+    np.testing.assert_array_equal(z[1], (-1.0) ** np.arange(n) / n)
+
+
+def test_batch_zero_and_one(cuda_device):
+    x = torch.empty(0, 64, device="cuda")
+    R.rdfft_fwd(x)
+    x = synth.randn((1, 64), seed=5).cuda()
+    xin = f64(x)
+    R.rdfft_fwd(x)
+    assert rel_l2_rows(f64(x), o.rdfft_fwd(xin)) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_guard_bands_untouched(dtype):
+    """Writes stay inside the transformed rows: canary rows around the
+    buffer and odd offsets into a larger allocation."""
+    for n in [8, 256, 4096]:
+        buf = torch.full((40, n), 7.25, dtype=synth.DTYPES[dtype], device="cuda")
+        inner = buf[3:37]
+        inner.copy_(synth.randn((34, n), seed=n, dtype=dtype).cuda())
+        R.rdfft_fwd(inner)
+        R.rdfft_inv(inner)
+        torch.cuda.synchronize()
+        assert (buf[:3] == 7.25).all() and (buf[37:] == 7.25).all()
+
+
+def test_zero_allocation():
+    """No device allocation per call: torch's allocator and cudaMemGetInfo unchanged."""
+    x = synth.randn((4096, 1024), seed=9, dtype="bf16").cuda()
+    w = synth.randn((3, 3, 256), seed=1, dtype="bf16").cuda()
+    xa = synth.randn((64, 768), seed=2, dtype="bf16").cuda()
+    ya = torch.empty_like(xa)
+    dw = torch.empty((3, 3, 256), dtype=torch.float32, device="cuda")
+    h = synth.randn((1, 1024), seed=3, dtype="bf16").cuda()
+
+    def calls():
+        R.rdfft_fwd(x)
+        R.rdfft_inv(x)
+        R.rdfft_packed_mul(x, h)
+        R.rdfft_packed_conjmul(x, h)
+        R.bca_fwd(xa, w, ya)
+        R.bca_bwd(xa, w, ya, ya, dw)
+
+    calls()  # lazy module loading happens on first launch, not per call
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    alloc0 = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    for _ in range(3):
+        calls()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert torch.cuda.memory_allocated() == alloc0
+    assert torch.cuda.max_memory_allocated() == alloc0
+    assert free1 == free0
+
+
+# ------------------------------------------------------------ packed products
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [2, 4, 16, 256, 1024, 4096])
+@pytest.mark.parametrize("conj", [False, True])
+@pytest.mark.parametrize("bcast", [False, True])
+def test_packed_mul_matches_oracle(n, dtype, conj, bcast):
+    b = 37
+    a = synth.randn((b, n), seed=n, dtype=dtype).cuda()
+    bb = synth.randn((1 if bcast else b, n), seed=n + 1, dtype=dtype).cuda()
+    ain, bin_ = f64(a), f64(bb)
+    (R.rdfft_packed_conjmul if conj else R.rdfft_packed_mul)(a, bb)
+    ref = (o.packed_conjmul if conj else o.packed_mul)(ain, bin_)
+    assert rel_l2_rows(f64(a), ref) <= (1e-6 if dtype == "f32" else 1e-2)
+
+
+def test_packed_mul_spec_examples(cuda_device):
+    a = torch.tensor([[10.0, -2, -2, 2]], device="cuda")
+    R.rdfft_packed_mul(a, a.clone())
+    assert a.cpu().tolist() == [[100.0, 0.0, 4.0, -8.0]]
+    a = torch.tensor([[10.0, -2, -2, 2]], device="cuda")
+    R.rdfft_packed_conjmul(a, a.clone())
+    assert a.cpu().tolist() == [[100.0, 8.0, 4.0, 0.0]]
+    x = torch.tensor([[1.0, 2, 3, 4]], device="cuda")
+    R.rdfft_fwd(x)
+    assert x.cpu().tolist() == [[10.0, -2.0, -2.0, 2.0]]
+    R.rdfft_inv(x)
+    assert x.cpu().tolist() == [[1.0, 2.0, 3.0, 4.0]]
+
+
+# ------------------------------------------------------------------ BCA layer
+BCA_SHAPES = [(1, 1, 2), (1, 1, 4), (2, 3, 8), (4, 2, 16), (3, 3, 64), (3, 3, 256), (4, 4, 1024), (2, 1, 4096)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("q_out,q_in,p", BCA_SHAPES)
+def test_bca_fwd_bwd_match_oracle(q_out, q_in, p, dtype):
+    T = 67
+    x, w, g = synth.bca_inputs(T, q_in * p, q_out * p, p, seed=p + q_in, dtype=dtype)
+    xc, wc, gc = x.cuda(), w.cuda(), g.cuda()
+    y = R.bca_fwd(xc, wc)
+    dx, dw = R.bca_bwd(xc, wc, gc)
+    torch.cuda.synchronize()
+    xo, wo, go = f64(x), f64(w), f64(g)
+    tol = TOL[dtype]
+    assert rel_l2_rows(f64(y), o.bca_fwd(xo, wo)) <= tol
+    dxo, dwo = o.bca_bwd(xo, wo, go)
+    assert rel_l2_rows(f64(dx), dxo) <= tol
+    # dw is fp32 accumulated over T tokens; judge it on the whole tensor
+    assert rel_l2_rows(f64(dw).reshape(1, -1), dwo.reshape(1, -1)) <= (1e-5 if dtype == "f32" else 2e-2)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_bca_bwd_dx_overwrites_g_in_place(dtype):
+    p, q = 256, 3
+    T = 50
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=3, dtype=dtype)
+    xc, wc, gc = x.cuda(), w.cuda(), g.cuda()
+    dx_ref, dw_ref = R.bca_bwd(xc, wc, gc.clone())
+    dw = torch.empty_like(dw_ref)
+    R.bca_bwd(xc, wc, gc, gc, dw)  # dx written over grad_output
+    torch.cuda.synchronize()
+    assert torch.equal(gc, dx_ref)
+    dxo, dwo = o.bca_bwd(f64(x), f64(w), f64(g))
+    assert rel_l2_rows(f64(gc), dxo) <= TOL[dtype]
+
+
+def test_bca_identity_and_shift(cuda_device):
+    p, q = 64, 2
+    w = torch.zeros(q, q, p)
+    for i in range(q):
+        w[i, i, 0] = 1
+    x = synth.randn((10, q * p), seed=4)
+    y = R.bca_fwd(x.cuda(), w.cuda())
+    assert rel_l2_rows(f64(y), f64(x)) < 1e-6
+    c = torch.zeros(1, 1, 4)
+    c[0, 0, 1] = 1  # c = [0,1,0,0] -> y = [x3, x0, x1, x2]
+    y = R.bca_fwd(torch.tensor([[5.0, 6, 7, 8]], device="cuda"), c.cuda())
+    assert np.allclose(f64(y), [[8, 5, 6, 7]], atol=1e-6)
+
+
+def test_bca_zero_grad_and_empty(cuda_device):
+    x, w, g = synth.bca_inputs(9, 512, 256, 256, seed=8, dtype="f32")
+    dx, dw = R.bca_bwd(x.cuda(), w.cuda(), torch.zeros_like(g).cuda())
+    assert not dx.any() and not dw.any()
+    dx, dw = R.bca_bwd(x[:0].cuda(), w.cuda(), g[:0].cuda())
+    assert dx.numel() == 0 and not dw.any()
+    y = R.bca_fwd(x[:0].cuda(), w.cuda())
+    assert y.numel() == 0
+
+
+def test_errors_raise(cuda_device):
+    with pytest.raises(R.RdfftError):
+        R.rdfft_fwd(torch.zeros(4, 12, device="cuda"))
+    with pytest.raises(TypeError):
+        R.rdfft_fwd(torch.zeros(4, 16, device="cuda", dtype=torch.float16))
+    with pytest.raises(ValueError):
+        R.rdfft_fwd(torch.zeros(4, 16))
