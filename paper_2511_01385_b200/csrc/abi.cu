@@ -10,7 +10,7 @@
 #include "../../include/rdfft.h"
 #include "bca_v1.cuh"
 #include "kernels_v1.cuh"
-#include "rdfft_kernels.cuh"
+#include "plan2.cuh"
 
 using namespace rdfft;
 
@@ -86,10 +86,11 @@ int packed(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, in
   if (overlap(a, batch * n * s, b, b_batch * n * s) && !(a == b && b_batch == batch)) return RDFFT_E_ALIAS;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logn = ilog2(n);
-  const int64_t items = batch * (n / 2);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)num_sms() * 16));
+  const int rows = (kPmTileBytes / (int)s) >> logn;
+  const int64_t tiles = (batch + rows - 1) / rows;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * 6));
 #define RDFFT_PM(T, C) \
-  packed_mul_kernel<T, C><<<grid, 256, 0, st>>>(static_cast<T*>(a), static_cast<const T*>(b), batch, (int)n, logn, b_batch)
+  packed_mul_kernel<T, C><<<grid, kPmThreads, 0, st>>>(static_cast<T*>(a), static_cast<const T*>(b), batch, (int)n, logn, b_batch)
   if (dtype == RDFFT_F32) {
     if (conj) RDFFT_PM(float, true); else RDFFT_PM(float, false);
   } else {

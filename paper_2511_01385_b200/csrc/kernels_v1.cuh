@@ -34,28 +34,63 @@ __global__ void __launch_bounds__(kV1Threads) rdfft_v1_kernel(T* __restrict__ x,
   }
 }
 
-// a <- a (.) b or a (.) conj(b) per bin; b broadcast when b_batch == 1.
+// a <- a (.) b or a (.) conj(b) per bin (P:L290-293); b broadcast when b_batch == 1.
+// One CTA row-loop: rows are staged through shared memory with 16-byte global accesses,
+// bins are combined from shared memory (slot k with slot n-k), then written back.
+constexpr int kPmThreads = 256;
+constexpr int kPmTileBytes = 16384;
+
 template <typename T, bool kConj>
-__global__ void __launch_bounds__(256) packed_mul_kernel(T* __restrict__ a, const T* __restrict__ b,
-                                                         int64_t batch, int n, int logn, int64_t b_batch) {
-  const int bins = (n >> 1);  // item k in [0, n/2): k = 0 handles slots 0 and n/2
-  const int64_t items = batch * bins;
-  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = it / bins;
-    const int k = (int)(it - v * bins);
-    T* ar = a + v * n;
-    const T* br = b + (b_batch == 1 ? 0 : v) * n;
-    if (k == 0) {
-      io<T>::st(ar, io<T>::ld(ar) * io<T>::ld(br));
-      if (n >= 2) io<T>::st(ar + bins, io<T>::ld(ar + bins) * io<T>::ld(br + bins));
-    } else {
-      const float2 A = make_float2(io<T>::ld(ar + k), io<T>::ld(ar + n - k));
-      const float2 B = make_float2(io<T>::ld(br + k), io<T>::ld(br + n - k));
-      const float2 C = kConj ? cmulc(A, B) : cmul(A, B);
-      io<T>::st(ar + k, C.x);
-      io<T>::st(ar + n - k, C.y);
+__global__ void __launch_bounds__(kPmThreads) packed_mul_kernel(T* __restrict__ a, const T* __restrict__ b,
+                                                                int64_t batch, int n, int logn, int64_t b_batch) {
+  constexpr int VEC = io<T>::kVec;
+  __shared__ __align__(16) unsigned char sa_raw[kPmTileBytes];
+  __shared__ __align__(16) unsigned char sb_raw[kPmTileBytes];
+  T* sa = reinterpret_cast<T*>(sa_raw);
+  T* sbv = reinterpret_cast<T*>(sb_raw);
+  const int rows = kPmTileBytes / (int)sizeof(T) >> logn;  // rows per tile (>= 1 for n <= 4096 f32)
+  const int64_t ntiles = (batch + rows - 1) / rows;
+  const bool bcast = (b_batch == 1);
+  const int half = n >> 1;
+  if (bcast) {  // the broadcast spectrum is staged once per CTA
+    for (int i = threadIdx.x; i < n; i += blockDim.x) sbv[i] = b[i];
+  }
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * rows;
+    const int nr = (int)(batch - r0 < rows ? batch - r0 : rows);
+    const int cnt = nr * n;
+    T* ag = a + r0 * n;
+    const T* bg = b + r0 * n;
+    __syncthreads();
+    const int nvec = (cnt % VEC == 0) ? cnt / VEC : 0;
+    for (int q = threadIdx.x; q < nvec; q += blockDim.x) {
+      reinterpret_cast<uint4*>(sa)[q] = __ldcs(reinterpret_cast<const uint4*>(ag) + q);
+      if (!bcast) reinterpret_cast<uint4*>(sbv)[q] = __ldcs(reinterpret_cast<const uint4*>(bg) + q);
     }
+    for (int i = nvec * VEC + threadIdx.x; i < cnt; i += blockDim.x) {
+      sa[i] = ag[i];
+      if (!bcast) sbv[i] = bg[i];
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < nr * half; it += blockDim.x) {
+      const int r = it >> (logn - 1), k = it & (half - 1);
+      T* ar = sa + (r << logn);
+      const T* br = sbv + (bcast ? 0 : (r << logn));
+      if (k == 0) {  // DC and Nyquist are real
+        io<T>::st(ar, io<T>::ld(ar) * io<T>::ld(br));
+        io<T>::st(ar + half, io<T>::ld(ar + half) * io<T>::ld(br + half));
+      } else {
+        const float2 A = make_float2(io<T>::ld(ar + k), io<T>::ld(ar + n - k));
+        const float2 B = make_float2(io<T>::ld(br + k), io<T>::ld(br + n - k));
+        const float2 C = kConj ? cmulc(A, B) : cmul(A, B);
+        io<T>::st(ar + k, C.x);
+        io<T>::st(ar + n - k, C.y);
+      }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nvec; q += blockDim.x)
+      __stcs(reinterpret_cast<uint4*>(ag) + q, reinterpret_cast<const uint4*>(sa)[q]);
+    for (int i = nvec * VEC + threadIdx.x; i < cnt; i += blockDim.x) ag[i] = sa[i];
   }
 }
 

@@ -1,0 +1,483 @@
+// plan2.cuh — register-blocked in-place rdFFT building blocks for sm_100a.
+//
+// Plan "2-pass" for n = R * M (R in {16, 32}, 4 <= M <= R):
+//
+//  pass 1 (stages m = 1 .. R/2 of the paper's schedule):
+//    After bit reversal, the first log2 R stages act independently on windows
+//    of R consecutive slots; window w holds the packed R-point spectrum of the
+//    decimated subsequence x[rev(w) :: n/R] (per-stage invariant, Eq. 6).  A
+//    thread loads two adjacent decimated subsequences 2c, 2c+1 (one 4-byte
+//    bf16x2 / 8-byte float2 access per element pair), runs the paper's stages
+//    in registers with compile-time twiddles, and writes windows rev(2c) and
+//    rev(2c) + S/2 (S = n/R).
+//
+//  last pass (stages m = R .. n/2): by Prop. 1 the four-slot groups of these
+//    log2 M stages close over S_k = {j R +- k}, so one
+//    thread owns S_k and finishes all remaining stages without exchange.  For
+//    1 <= k <= R/2 the stages are regrouped as a twiddle W_n^{k rev(j)} on the
+//    M block spectra Z_j(k) followed by an M-point complex DIT FFT (the same
+//    radix-2 butterflies, reordered; k = R/2 has zero imaginary input).  The
+//    block DCs (slots j R) form a real M-point FFT run by one lane per vector
+//    of the last warp.
+//
+//  Intermediate: fp32 "half pairs" in shared memory, H[q] = (slot q, slot
+//  q + n/2), 16-byte pad per R-window (conflict-free 128-bit window writes;
+//  the pad also holds the zero imaginary input of lane k = R/2) and a per-row
+//  skew.  Every shared access is 8 or 16 bytes, every address is a per-thread
+//  base plus a compile-time offset.
+//
+//  Inverse: the reversed graph (Eq. 7) — last pass first
+//  (conjugate twiddles; 1/n folded into its table, reading C4), then the
+//  paper's inverse stages in pass 1.
+#pragma once
+
+#include "common.cuh"
+#include "regfft.cuh"
+
+namespace rdfft {
+
+// 2^16 as a constant-bank operand ptxas cannot fold: u * kTwo16 (= u << 16) then issues as
+// IMAD on the full-rate FMA pipe instead of SHF on the half-rate ALU pipe.
+__constant__ uint32_t kTwo16 = 65536u;
+
+template <typename T>
+struct sio;  // shared-memory pair loads of T (staging buffers)
+template <>
+struct sio<float> {
+  __device__ __forceinline__ static float2 ld2(const float* p, uint32_t) {
+    return *reinterpret_cast<const float2*>(p);
+  }
+};
+template <>
+struct sio<__nv_bfloat16> {
+  __device__ __forceinline__ static float2 ld2(const __nv_bfloat16* p, uint32_t k65536) {
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(p);
+    return make_float2(__uint_as_float(u * k65536), __uint_as_float(u & 0xffff0000u));
+  }
+};
+
+template <typename T>
+struct gio;  // global pair stores (streaming)
+template <>
+struct gio<float> {
+  __device__ __forceinline__ static void st2(float* p, float2 v) { __stcs(reinterpret_cast<float2*>(p), v); }
+};
+template <>
+struct gio<__nv_bfloat16> {
+  __device__ __forceinline__ static void st2(__nv_bfloat16* p, float2 v) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
+    __stcs(reinterpret_cast<unsigned int*>(p), *reinterpret_cast<unsigned int*>(&h));
+  }
+};
+
+template <typename T, int N_, int R_, int VT_>
+struct Plan2 {
+  using elem = T;
+  static constexpr int N = N_, R = R_, VT = VT_;
+  static constexpr int LN = ilog2c<N>();
+  static constexpr int LR = ilog2c<R>();
+  static constexpr int M = N / R;           // last-pass FFT size (blocks per vector)
+  static constexpr int LM = ilog2c<M>();
+  static constexpr int S = N / R;           // decimated subsequences per vector
+  static constexpr int LS = ilog2c<S>();
+  static constexpr int P1 = S / 2;          // pass-1 threads per vector
+  static constexpr int LPV = R / 2;         // last-pass lanes per vector: k = 1 .. R/2
+  static constexpr int NT = VT * LPV;
+  static constexpr int WSTR = R + 2;        // float2 per window (+16 B pad)
+  static constexpr int NWIN = S / 2;        // windows per row (first half of the slots)
+  static constexpr int ROWA = ((NWIN * WSTR + 14 + 15) / 16) * 16;  // room for the row skew (<= 14)
+  static constexpr int HF = VT * ROWA + 16;  // float2 in one H region
+  static constexpr int TWF = M * LPV;
+  static constexpr int CHV = N / 4;         // 16-byte H chunks per vector
+  static constexpr int STAGE = VT * N * (int)sizeof(T);
+  static_assert(M <= R && M >= 4 && (R == 32 || R == 16), "2-pass plan shape");
+  static_assert(NT % 32 == 0 && VT * P1 <= NT, "thread mapping");
+  static_assert(VT <= 32, "one DC-set lane per vector in the last warp");
+  static_assert((VT * CHV) % NT == 0, "chunk mapping");
+
+  // Row skew (float2): 16 lanes of one vector (R = 32) or two vectors (R = 16) share a
+  // shared-memory phase in the last pass; the DC warp has one lane per vector.
+  __host__ __device__ static constexpr int skew(int v) {
+    return LPV == 16 ? 2 * (v & 7) : (v & 1) * 8 + ((v >> 1) & 3) * 2;
+  }
+  __host__ __device__ static constexpr int row(int v) { return v * ROWA + skew(v); }
+  // float2 offset of logical half-pair index q (0 <= q < N/2) of vector v
+  __host__ __device__ static constexpr int hidx(int v, int q) { return row(v) + (q / R) * WSTR + (q % R); }
+};
+
+// Per-thread role pointers of one thread group (lt = thread index inside the group).
+template <typename P>
+struct P2Roles {
+  float2* h1;        // pass 1: window w1 of vector v1
+  int v1, s1;        //   element offset of subsequence 2 c1 in a tile
+  bool act1;
+  int v2, k;         // last pass: vector v2, set k
+  float2* ha;        //   slots j R + k
+  float2* hm;        //   slots (j+1) R - k
+  float2* hmz;       //   imaginary input (fwd) / output (inv): pad for k = R/2
+  const float2* twf; //   forward twiddles (column k - 1)
+  const float2* twi; //   inverse twiddles
+  int dv;            // DC set: lane dv of the last warp (dv < 0: none)
+  float2* hd;
+  int vq, tq;        // chunk phase: per-thread vector / chunk offsets
+  float2* hq;
+
+  __device__ __forceinline__ P2Roles(float2* H, const float2* TWf, const float2* TWi, int lt) {
+    constexpr int R = P::R;
+    v1 = lt / P::P1;
+    const int w1 = lt % P::P1;
+    const int c1 = rev_bits<P::LS - 1>(w1);  // rev_LS(2 c1) == w1: lane order = window order
+    act1 = lt < P::VT * P::P1;
+    h1 = H + P::row(v1) + w1 * P::WSTR;
+    s1 = v1 * P::N + 2 * c1;
+    v2 = lt / P::LPV;
+    k = 1 + lt % P::LPV;
+    ha = H + P::row(v2) + k;
+    hm = H + P::row(v2) + (R - k);
+    hmz = (k == R / 2) ? (H + P::row(v2) + R) : hm;
+    twf = TWf + (k - 1);
+    twi = TWi + (k - 1);
+    dv = lt - (P::NT - 32);
+    hd = H + P::row(dv < 0 ? 0 : dv);
+    vq = (P::CHV < P::NT) ? lt / P::CHV : 0;
+    tq = (P::CHV < P::NT) ? lt % P::CHV : lt;
+    hq = H + P::row(vq) + (2 * tq / R) * P::WSTR + (2 * tq) % R;
+  }
+};
+
+// Twiddle tables and pads (whole CTA): TWf[j LPV + k-1] = W_N^{k rev(j)}, TWi = conj(.)/N.
+template <typename P>
+__device__ __forceinline__ void p2_tables(float2* TWf, float2* TWi, int tid, int nthreads) {
+  for (int e = tid; e < P::TWF; e += nthreads) {
+    const int j = e / P::LPV, k = 1 + e % P::LPV;
+    float s, c;
+    sincospif(2.0f * (float)(k * rev_bits<P::LM>(j)) / (float)P::N, &s, &c);
+    if (TWf) TWf[e] = make_float2(c, -s);
+    if (TWi) TWi[e] = make_float2(c * (1.0f / P::N), s * (1.0f / P::N));
+  }
+}
+template <typename P>
+__device__ __forceinline__ void p2_zero_pads(float2* H, int nvec, int tid, int nthreads) {
+  for (int e = tid; e < P::NWIN * nvec; e += nthreads) {
+    float2* pad = H + P::row(e / P::NWIN) + (e % P::NWIN) * P::WSTR + P::R;
+    pad[0] = make_float2(0.f, 0.f);
+    pad[1] = make_float2(0.f, 0.f);
+  }
+}
+
+// ---------------------------------------------------------------- forward pieces
+// pass 1 from a staged tile (shared memory, natural order, element type T)
+template <typename P>
+__device__ __forceinline__ void p2_pass1_fwd(const P2Roles<P>& r, const typename P::elem* st, int nv,
+                                             uint32_t k65536) {
+  using T = typename P::elem;
+  constexpr int R = P::R, S = P::S;
+  if (r.act1 && r.v1 < nv) {
+    float2 b[R];
+    const T* src = st + r.s1;
+    ct::static_for<0, R>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      b[rev_bits<P::LR>(i)] = sio<T>::ld2(src + S * i, k65536);
+    });
+    rfft_fwd_reg<R>(b);
+    ct::static_for<0, R / 2>([&](auto I) {
+      constexpr int i = 2 * decltype(I)::value;
+      *reinterpret_cast<float4*>(r.h1 + i) = make_float4(b[i].x, b[i].y, b[i + 1].x, b[i + 1].y);
+    });
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void p2_last_fwd(const P2Roles<P>& r, int nv) {
+  constexpr int M = P::M, WSTR = P::WSTR;
+  if (r.v2 < nv) {
+    float zr[M], zi[M];
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      const float2 a = r.ha[jj * WSTR];
+      const float2 bb = r.hmz[jj * WSTR];
+      zr[jj] = a.x;
+      zr[jj + M / 2] = a.y;
+      zi[jj] = bb.x;
+      zi[jj + M / 2] = bb.y;
+    });
+    ct::static_for<1, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      const float2 t = r.twf[j * P::LPV];
+      const float q = zr[j];
+      zr[j] = fmaf(q, t.x, -zi[j] * t.y);
+      zi[j] = fmaf(q, t.y, zi[j] * t.x);
+    });
+    cfft_dit<M>(zr, zi);
+    ct::static_for<0, M / 2>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      r.ha[q * WSTR] = make_float2(zr[q], -zi[q + M / 2]);
+      r.hm[(M / 2 - 1 - q) * WSTR] = make_float2(zr[q + M / 2], zi[q]);
+    });
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void p2_dc_fwd(const P2Roles<P>& r, int nv) {
+  constexpr int M = P::M, WSTR = P::WSTR;
+  if (r.dv >= 0 && r.dv < nv) {  // block DCs j R: packed real M-point DFT (input already bit-reversed)
+    float d[M];
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      const float2 a = r.hd[jj * WSTR];
+      d[jj] = a.x;
+      d[jj + M / 2] = a.y;
+    });
+    rfft_fwd_reg<M>(d);
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      r.hd[jj * WSTR] = make_float2(d[jj], d[jj + M / 2]);
+    });
+  }
+}
+
+// Visit this thread's 16-byte H chunks: f(vv, t, h) with vv the vector, t the chunk index
+// (slots 2t, 2t+1 and +N/2) and h the chunk's float2 address.  Chunk (vv, t) lives at
+// row(vv) + (2t / R) WSTR + 2t % R; the per-thread base hq covers (vq, tq).
+template <typename P, typename F>
+__device__ __forceinline__ void p2_chunks(const P2Roles<P>& r, F&& f) {
+  constexpr int CPT = P::VT * P::CHV / P::NT;
+  ct::static_for<0, CPT>([&](auto RR) {
+    constexpr int rr = decltype(RR)::value;
+    if constexpr (P::CHV >= P::NT) {  // one vector per step; vq == 0, compile-time offsets
+      constexpr int v = rr / (P::CHV / P::NT);
+      constexpr int toff = P::NT * (rr % (P::CHV / P::NT));
+      f(v, r.tq + toff, r.hq + P::row(v) + (2 * toff / P::R) * P::WSTR);
+    } else {  // NT / CHV vectors per step: the row skew difference is a runtime term
+      constexpr int v = rr * (P::NT / P::CHV);
+      const int vv = r.vq + v;
+      f(vv, r.tq, r.hq + v * P::ROWA + P::skew(vv) - P::skew(r.vq));
+    }
+  });
+}
+
+// H (packed spectra, half pairs) -> global tile (natural order)
+template <typename P>
+__device__ __forceinline__ void p2_store(const P2Roles<P>& r, typename P::elem* dst, int nv) {
+  using T = typename P::elem;
+  p2_chunks<P>(r, [&](int vv, int t, const float2* h) {
+    if (vv < nv) {
+      const float4 f = *reinterpret_cast<const float4*>(h);
+      T* d = dst + vv * P::N + 2 * t;
+      gio<T>::st2(d, make_float2(f.x, f.z));
+      gio<T>::st2(d + P::N / 2, make_float2(f.y, f.w));
+    }
+  });
+}
+
+// ---------------------------------------------------------------- inverse pieces
+// staged tile (natural order) -> H half pairs
+template <typename P>
+__device__ __forceinline__ void p2_load(const P2Roles<P>& r, const typename P::elem* st, int nv, uint32_t k65536) {
+  using T = typename P::elem;
+  p2_chunks<P>(r, [&](int vv, int t, const float2* h) {
+    if (vv < nv) {
+      const T* src = st + vv * P::N + 2 * t;
+      const float2 lo = sio<T>::ld2(src, k65536);
+      const float2 hi = sio<T>::ld2(src + P::N / 2, k65536);
+      *reinterpret_cast<float4*>(const_cast<float2*>(h)) = make_float4(lo.x, hi.x, lo.y, hi.y);
+    }
+  });
+}
+
+template <typename P>
+__device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv) {
+  constexpr int M = P::M, WSTR = P::WSTR, LM = P::LM;
+  if (r.v2 < nv) {
+    // Y[q] is loaded into register rev(q); a DIT pass with conjugate twiddles then leaves
+    // out[p] = M x IDFT(Y)[p] in register p, and Z'_j = IDFT(Y)[rev(j)] sits in register rev(j).
+    float zr[M], zi[M];
+    ct::static_for<0, M / 2>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      const float2 a = r.ha[q * WSTR];                    // (Re Y[q], -Im Y[q + M/2])
+      const float2 bb = r.hm[(M / 2 - 1 - q) * WSTR];     // (Re Y[q + M/2], Im Y[q])
+      zr[rev_bits<LM>(q)] = a.x;
+      zi[rev_bits<LM>(q + M / 2)] = -a.y;
+      zr[rev_bits<LM>(q + M / 2)] = bb.x;
+      zi[rev_bits<LM>(q)] = bb.y;
+    });
+    cfft_dit<M, true>(zr, zi);
+    ct::static_for<0, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int rj = rev_bits<LM>(j);
+      const float2 t = r.twi[j * P::LPV];
+      const float q = zr[rj];
+      zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
+      zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
+    });
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      constexpr int r1 = rev_bits<LM>(jj), r2 = rev_bits<LM>(jj + M / 2);
+      r.ha[jj * WSTR] = make_float2(zr[r1], zr[r2]);
+      r.hmz[jj * WSTR] = make_float2(zi[r1], zi[r2]);  // k = R/2: imaginary part discarded into the pad
+    });
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void p2_dc_inv(const P2Roles<P>& r, int nv) {
+  constexpr int M = P::M, WSTR = P::WSTR;
+  if (r.dv >= 0 && r.dv < nv) {
+    float d[M];
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      const float2 a = r.hd[jj * WSTR];
+      d[jj] = a.x;
+      d[jj + M / 2] = a.y;
+    });
+    rfft_inv_reg<M>(d);
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      r.hd[jj * WSTR] = make_float2(d[jj] * (1.0f / P::N), d[jj + M / 2] * (1.0f / P::N));
+    });
+  }
+}
+
+// inverse pass 1: H windows -> real signals in global memory
+template <typename P>
+__device__ __forceinline__ void p2_pass1_inv(const P2Roles<P>& r, typename P::elem* dst_tile, int nv) {
+  using T = typename P::elem;
+  constexpr int R = P::R, S = P::S;
+  if (r.act1 && r.v1 < nv) {
+    float2 b[R];
+    ct::static_for<0, R / 2>([&](auto I) {
+      constexpr int i = 2 * decltype(I)::value;
+      const float4 f = *reinterpret_cast<const float4*>(r.h1 + i);
+      b[i] = make_float2(f.x, f.y);
+      b[i + 1] = make_float2(f.z, f.w);
+    });
+    rfft_inv_reg<R>(b);
+    T* dst = dst_tile + r.s1;
+    ct::static_for<0, R>([&](auto I) {
+      constexpr int i = decltype(I)::value;
+      gio<T>::st2(dst + S * i, b[rev_bits<P::LR>(i)]);
+    });
+  }
+}
+
+// ---------------------------------------------------------------- TMA staging
+template <typename T>
+__device__ __forceinline__ void stage_issue(const T* src, uint32_t bytes, void* dst, uint64_t* bar) {
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(bar, bytes);
+  bulk_g2s(dst, src, bytes, bar);
+}
+
+// ---------------------------------------------------------------- rdfft kernels
+template <typename P>
+struct P2Smem {  // [stage 0][stage 1][H][TW][bars]
+  static constexpr size_t H_OFF = 2 * (size_t)P::STAGE;
+  static constexpr size_t TW_OFF = H_OFF + (size_t)P::HF * 8;
+  static constexpr size_t BAR_OFF = TW_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BYTES = BAR_OFF + 16;
+};
+
+template <typename P, bool kInv>
+__global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restrict__ x, int64_t batch) {
+  using T = typename P::elem;
+  using L = P2Smem<P>;
+  constexpr int VT = P::VT, N = P::N;
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  float2* H = reinterpret_cast<float2*>(base + L::H_OFF);
+  float2* TW = reinterpret_cast<float2*>(base + L::TW_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
+  const int tid = threadIdx.x;
+  p2_tables<P>(kInv ? nullptr : TW, kInv ? TW : nullptr, tid, P::NT);
+  if (!kInv) p2_zero_pads<P>(H, VT, tid, P::NT);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  const P2Roles<P> r(H, TW, TW, tid);
+  const uint32_t k65536 = kTwo16;
+  const int64_t ntiles = (batch + VT - 1) / VT;
+  auto tile_bytes = [&](int64_t t) {
+    const int64_t nv = batch - t * VT < VT ? batch - t * VT : VT;
+    return (uint32_t)(nv * N * (int)sizeof(T));
+  };
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 0; q < 2; ++q) {
+      const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
+      if (t < ntiles) stage_issue(x + t * VT * (int64_t)N, tile_bytes(t), base + q * P::STAGE, bar + q);
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
+    T* xt = x + tile * VT * (int64_t)N;
+    const int sb = it & 1;
+    const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
+    const int64_t nxt = tile + 2 * (int64_t)gridDim.x;
+    mbar_wait(bar + sb, (it >> 1) & 1);
+    if (!kInv) {
+      p2_pass1_fwd<P>(r, st, nv, k65536);
+      __syncthreads();  // H complete; staging buffer sb consumed
+      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+      p2_last_fwd<P>(r, nv);
+      p2_dc_fwd<P>(r, nv);
+      __syncthreads();
+      p2_store<P>(r, xt, nv);
+    } else {
+      p2_load<P>(r, st, nv, k65536);
+      __syncthreads();
+      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+      p2_last_inv<P>(r, nv);
+      p2_dc_inv<P>(r, nv);
+      __syncthreads();
+      p2_pass1_inv<P>(r, xt, nv);
+    }
+    __syncthreads();  // H free for the next tile
+  }
+}
+
+template <typename P>
+bool launch_plan2(typename P::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
+  using L = P2Smem<P>;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
+  auto kf = rdfft2_kernel<P, false>;
+  auto ki = rdfft2_kernel<P, true>;
+  static bool configured = false;
+  static int per_sm = 1;
+  if (!configured) {
+    for (auto k : {kf, ki}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    }
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kf, P::NT, L::BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ki, P::NT, L::BYTES);
+    per_sm = a < b ? a : b;
+    if (per_sm < 1) per_sm = 1;
+    configured = true;
+  }
+  const int64_t tiles = (batch + P::VT - 1) / P::VT;
+  const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
+  if (inverse)
+    ki<<<grid, P::NT, L::BYTES, st>>>(x, batch);
+  else
+    kf<<<grid, P::NT, L::BYTES, st>>>(x, batch);
+  return true;
+}
+
+// Returns true when a specialised kernel was launched for (n, T).
+template <typename T>
+bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st) {
+  (void)logn;
+  switch (n) {
+    case 128: return launch_plan2<Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
+    case 256: return launch_plan2<Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
+    case 512: return launch_plan2<Plan2<T, 512, 32, 8>>(x, batch, inverse, sms, st);
+    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8>>(x, batch, inverse, sms, st);
+    default: return false;
+  }
+}
+
+}  // namespace rdfft
