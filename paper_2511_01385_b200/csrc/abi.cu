@@ -11,6 +11,7 @@
 #include "bca_v1.cuh"
 #include "kernels_v1.cuh"
 #include "plan2.cuh"
+#include "bca2.cuh"
 
 using namespace rdfft;
 
@@ -153,6 +154,13 @@ int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int6
   if (smem > 227 * 1024) return RDFFT_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logp = ilog2(p);
+  const bool fast =
+      dtype == RDFFT_F32
+          ? bca_fwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w), static_cast<float*>(y), T,
+                                q_in, q_out, (int)p, num_sms(), st)
+          : bca_fwd_fast<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+                                        static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, num_sms(), st);
+  if (fast) return launched();
   if (dtype == RDFFT_F32) {
     auto k = bca_fwd_v1_kernel<float>;
     const int grid = grid_for(k, kBcaThreads, smem, T);
@@ -193,7 +201,18 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(dw, 0, nw * sizeof(float), st) != cudaSuccess) return RDFFT_E_CUDA;
   const int logp = ilog2(p);
-  if (T > 0) {
+  const bool fast =
+      T > 0 && (dtype == RDFFT_F32
+                    ? bca_bwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w),
+                                          static_cast<const float*>(g), static_cast<float*>(dx), dw, T, q_in, q_out,
+                                          (int)p, num_sms(), st)
+                    : bca_bwd_fast<__nv_bfloat16>(
+                          static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+                          static_cast<const __nv_bfloat16*>(g), static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out,
+                          (int)p, num_sms(), st));
+  if (fast) {
+    if ((rc = launched()) != RDFFT_OK) return rc;
+  } else if (T > 0) {
     if (dtype == RDFFT_F32) {
       auto k = bca_bwd_v1_kernel<float>;
       const int grid = grid_for(k, kBcaThreads, smem, T);

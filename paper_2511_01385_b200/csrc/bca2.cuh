@@ -1,0 +1,444 @@
+// bca2.cuh — fused block-circulant adapter (BCA) forward / backward on the
+// register-blocked 2-pass transform (plan2.cuh); square layers (q_in == q_out
+// = q <= 4), p in {256, 512, 1024}.
+//
+// Forward (Eq. 4; blocks P:L184), per tile of TT tokens
+// (TT q consecutive p-blocks = one contiguous tile of the activation):
+//   X = rdFFT(x) in shared memory -> Y_i = sum_j W_ij (.) X_j in place ->
+//   y = IrdFFT(Y) straight to HBM.
+// W_ij = rdFFT(w_ij) is computed once per CTA into a resident shared-memory
+// region with the same half-pair layout (reading C12); x is never written (C13).
+//
+// Backward (Eq. 5; pairing C11), per tile:
+//   X = rdFFT(x), G = rdFFT(g) (two thread groups, one per operand)
+//   Acc_ij += conj(X_j) (.) G_i     per-thread fp32 registers for the CTA's whole token range
+//   D_j = sum_i conj(W_ij) (.) G_i  in place of X_j,  dx = IrdFFT(D)  (dx may alias g)
+// then Acc is added to dw with fp32 atomics; dw is zeroed before and
+// inverse-transformed after (dw finalize launch), in fp32.
+//
+// Product layout: item u < N/4 owns half-pair positions u and N/2 - u, i.e. the
+// complex bins u and N/2 - u:  bin u = (H[u].x, H[N/2-u].y), bin N/2-u = (H[N/2-u].x, H[u].y).
+// Item 0 owns H[0] = (DC, Nyquist) (two real bins) and H[N/4] = bin N/4.
+#pragma once
+
+#include "plan2.cuh"
+
+namespace rdfft {
+
+constexpr int kBcaQMax = 4;
+
+template <typename P>
+struct BcaFwdSmem {  // [stage x STAGES][H][W][TWf][TWi][bars]
+  static constexpr int STAGES = sizeof(typename P::elem) == 2 ? 2 : 1;
+  static constexpr int WF = kBcaQMax * kBcaQMax * P::ROWA + 16;
+  static constexpr size_t H_OFF = (size_t)STAGES * P::STAGE;
+  static constexpr size_t W_OFF = H_OFF + (size_t)P::HF * 8;
+  static constexpr size_t TWF_OFF = W_OFF + (size_t)WF * 8;
+  static constexpr size_t TWI_OFF = TWF_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BAR_OFF = TWI_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BYTES = BAR_OFF + 16;
+};
+
+// complex helpers on float2 (re, im)
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 c) {  // c + a b
+  return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 c) {  // c + conj(a) b
+  return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(-a.y, b.x, c.y)));
+}
+__device__ __forceinline__ float2 rfma(float2 a, float2 b, float2 c) {  // componentwise c + a b
+  return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+
+// Gather the two bins of item u from the half pairs at positions (pa, pb) of one row.
+struct BinPair {
+  float2 b1, b2;
+};
+__device__ __forceinline__ BinPair bins_get(const float2* rowbase, int oa, int ob, bool special) {
+  const float2 a = rowbase[oa], b = rowbase[ob];
+  if (special) return {a, b};                                    // (DC, Nyq) and bin N/4
+  return {make_float2(a.x, b.y), make_float2(b.x, a.y)};
+}
+__device__ __forceinline__ void bins_put(float2* rowbase, int oa, int ob, bool special, BinPair v) {
+  if (special) {
+    rowbase[oa] = v.b1;
+    rowbase[ob] = v.b2;
+  } else {
+    rowbase[oa] = make_float2(v.b1.x, v.b2.y);
+    rowbase[ob] = make_float2(v.b2.x, v.b1.y);
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void bca_item_offsets(int u, int& oa, int& ob) {
+  // physical float2 offsets (relative to a row) of half-pair positions of item u
+  constexpr int R = P::R, W = P::WSTR, HALF = P::N / 2;
+  const int qa = u, qb = (u == 0) ? P::N / 4 : HALF - u;
+  oa = (qa / R) * W + qa % R;
+  ob = (qb / R) * W + qb % R;
+}
+
+// In-place forward product over one tile: Y_i = sum_j W_ij (.) X_j for tokens of this tile.
+template <typename P>
+__device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int q, int ntok, int tid) {
+  constexpr int NI = P::N / 4;
+  constexpr int TS = P::NT >= NI ? P::NT / NI : 1;  // thread groups sharing an item (token split)
+  for (int u = tid % NI; u < NI; u += (P::NT >= NI ? NI : P::NT)) {
+    const int ts = P::NT >= NI ? tid / NI : 0;
+    int oa, ob;
+    bca_item_offsets<P>(u, oa, ob);
+    const bool special = (u == 0);
+    BinPair w[kBcaQMax][kBcaQMax];
+#pragma unroll
+    for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+      for (int j = 0; j < kBcaQMax; ++j)
+        if (i < q && j < q) w[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
+    for (int tt = ts; tt < ntok; tt += TS) {
+      BinPair x[kBcaQMax];
+#pragma unroll
+      for (int j = 0; j < kBcaQMax; ++j)
+        if (j < q) x[j] = bins_get(H + P::row(tt * q + j), oa, ob, special);
+#pragma unroll
+      for (int i = 0; i < kBcaQMax; ++i) {
+        if (i < q) {
+          BinPair y = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int j = 0; j < kBcaQMax; ++j) {
+            if (j < q) {
+              y.b1 = special ? rfma(w[i][j].b1, x[j].b1, y.b1) : cfma(w[i][j].b1, x[j].b1, y.b1);
+              y.b2 = cfma(w[i][j].b2, x[j].b2, y.b2);
+            }
+          }
+          bins_put(H + P::row(tt * q + i), oa, ob, special, y);
+        }
+      }
+    }
+  }
+}
+
+template <typename P>
+__global__ void __launch_bounds__(P::NT) bca_fwd2_kernel(const typename P::elem* __restrict__ x,
+                                                         const typename P::elem* __restrict__ w,
+                                                         typename P::elem* __restrict__ y, int64_t T_, int q) {
+  using T = typename P::elem;
+  using L = BcaFwdSmem<P>;
+  constexpr int N = P::N;
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  float2* H = reinterpret_cast<float2*>(base + L::H_OFF);
+  float2* Wr = reinterpret_cast<float2*>(base + L::W_OFF);
+  float2* TWf = reinterpret_cast<float2*>(base + L::TWF_OFF);
+  float2* TWi = reinterpret_cast<float2*>(base + L::TWI_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
+  const int tid = threadIdx.x;
+  const int TT = P::VT / q;                 // tokens per tile
+  const int64_t ntiles = (T_ + TT - 1) / TT;
+  const int64_t tok_elems = (int64_t)q * N;  // elements per token row (d = q p)
+  p2_tables<P>(TWf, TWi, tid, P::NT);
+  p2_zero_pads<P>(H, P::VT, tid, P::NT);
+  p2_zero_pads<P>(Wr, q * q, tid, P::NT);
+  if (tid == 0) {
+    for (int s = 0; s < L::STAGES; ++s) mbar_init(bar + s, 1);
+    fence_mbar_init();
+  }
+  const uint32_t k65536 = kTwo16;
+  const P2Roles<P> rh(H, TWf, TWi, tid);
+  auto tile_bytes = [&](int64_t t) {
+    const int64_t nt = T_ - t * TT < TT ? T_ - t * TT : TT;
+    return (uint32_t)(nt * tok_elems * (int)sizeof(T));
+  };
+  __syncthreads();
+  // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors, into the resident region
+  if (tid == 0) stage_issue(w, (uint32_t)(q * q * N * (int)sizeof(T)), base, bar);
+  mbar_wait(bar, 0);
+  {
+    const P2Roles<P> rw(Wr, TWf, TWi, tid);
+    p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(base), q * q, k65536);
+    __syncthreads();
+    p2_last_fwd<P>(rw, q * q);
+    p2_dc_fwd<P>(rw, q * q);
+  }
+  __syncthreads();
+  uint32_t phase_use[2] = {1, 0};  // stage 0 has completed one phase (the weights)
+  if (tid == 0) {
+    for (int s = 0; s < L::STAGES; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ntiles) stage_issue(x + t * TT * tok_elems, tile_bytes(t), base + s * P::STAGE, bar + s);
+    }
+  }
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
+    const int nv = ntok * q;
+    const int sb = L::STAGES == 2 ? (it & 1) : 0;
+    const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
+    mbar_wait(bar + sb, phase_use[sb] & 1);
+    ++phase_use[sb];
+    p2_pass1_fwd<P>(rh, st, nv, k65536);
+    __syncthreads();  // H complete, staging sb consumed
+    const int64_t nxt = tile + (int64_t)L::STAGES * gridDim.x;
+    if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * TT * tok_elems, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+    p2_last_fwd<P>(rh, nv);
+    p2_dc_fwd<P>(rh, nv);
+    __syncthreads();
+    bca_product_fwd<P>(H, Wr, q, ntok, tid);
+    __syncthreads();
+    p2_last_inv<P>(rh, nv);
+    p2_dc_inv<P>(rh, nv);
+    __syncthreads();
+    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ backward
+template <typename P>
+struct BcaBwdSmem {  // [sx x STAGES][sg x STAGES][Hx][Hg][W][TWf][TWi][bars x 2 STAGES]
+  static constexpr int STAGES = sizeof(typename P::elem) == 2 ? 2 : 1;
+  static constexpr int WF = kBcaQMax * kBcaQMax * P::ROWA + 16;
+  static constexpr size_t SG_OFF = (size_t)STAGES * P::STAGE;
+  static constexpr size_t HX_OFF = 2 * (size_t)STAGES * P::STAGE;
+  static constexpr size_t HG_OFF = HX_OFF + (size_t)P::HF * 8;
+  static constexpr size_t W_OFF = HG_OFF + (size_t)P::HF * 8;
+  static constexpr size_t TWF_OFF = W_OFF + (size_t)WF * 8;
+  static constexpr size_t TWI_OFF = TWF_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BAR_OFF = TWI_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BYTES = BAR_OFF + 32;
+};
+
+template <typename P>
+__global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::elem* __restrict__ x,
+                                                             const typename P::elem* __restrict__ w,
+                                                             const typename P::elem* g, typename P::elem* dx,
+                                                             float* __restrict__ dw, int64_t T_, int q) {
+  using T = typename P::elem;
+  using L = BcaBwdSmem<P>;
+  constexpr int N = P::N, NT2 = 2 * P::NT, NI = N / 4;
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  float2* Hx = reinterpret_cast<float2*>(base + L::HX_OFF);
+  float2* Hg = reinterpret_cast<float2*>(base + L::HG_OFF);
+  float2* Wr = reinterpret_cast<float2*>(base + L::W_OFF);
+  float2* TWf = reinterpret_cast<float2*>(base + L::TWF_OFF);
+  float2* TWi = reinterpret_cast<float2*>(base + L::TWI_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);  // [x s0, x s1, g s0, g s1]
+  const int tid = threadIdx.x;
+  const int grp = tid / P::NT, lt = tid % P::NT;  // group 0: x operand, group 1: g operand
+  const int TT = P::VT / q;
+  const int64_t ntiles = (T_ + TT - 1) / TT;
+  const int64_t tok_elems = (int64_t)q * N;
+  unsigned char* stg = base + (grp ? L::SG_OFF : 0);
+  uint64_t* gbar = bar + grp * 2;
+  const T* src = grp ? g : x;
+  float2* Hm = grp ? Hg : Hx;
+  p2_tables<P>(TWf, TWi, tid, NT2);
+  p2_zero_pads<P>(Hx, P::VT, tid, NT2);
+  p2_zero_pads<P>(Hg, P::VT, tid, NT2);
+  p2_zero_pads<P>(Wr, q * q, tid, NT2);
+  if (tid == 0) {
+    for (int s = 0; s < 4; ++s) mbar_init(bar + s, 1);
+    fence_mbar_init();
+  }
+  const uint32_t k65536 = kTwo16;
+  const P2Roles<P> rh(Hm, TWf, TWi, lt);
+  auto tile_bytes = [&](int64_t t) {
+    const int64_t nt = T_ - t * TT < TT ? T_ - t * TT : TT;
+    return (uint32_t)(nt * tok_elems * (int)sizeof(T));
+  };
+  __syncthreads();
+  // ---- prologue: W_ij = rdFFT(w_ij) into the resident region.  q*q <= VT: group 0 does all
+  // rows; q*q = 16 > VT = 8: rows [0, 8) by group 0 and [8, 16) by group 1 (8 = skew period,
+  // so row(8 + v) == 8 ROWA + row(v)).
+  const int nw = q * q;
+  const int half = nw <= P::VT ? nw : 8;
+  const int w0 = grp ? half : 0, wn = grp ? nw - half : half;
+  if (lt == 0 && wn > 0) stage_issue(w + (int64_t)w0 * N, (uint32_t)(wn * N * (int)sizeof(T)), stg, gbar);
+  if (wn > 0) mbar_wait(gbar, 0);
+  {
+    const P2Roles<P> rw(Wr + w0 * P::ROWA, TWf, TWi, lt);
+    p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(stg), wn, k65536);
+    __syncthreads();
+    p2_last_fwd<P>(rw, wn);
+    p2_dc_fwd<P>(rw, wn);
+  }
+  __syncthreads();
+  uint32_t phase_use[2] = {wn > 0 ? 1u : 0u, 0};
+  if (lt == 0) {
+    for (int s = 0; s < L::STAGES; ++s) {
+      const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+      if (t < ntiles) stage_issue(src + t * TT * tok_elems, tile_bytes(t), stg + s * P::STAGE, gbar + s);
+    }
+  }
+  // dW accumulators: item u = tid (one item per thread when 2 NT == N/4), all q*q pairs, 2 bins
+  static_assert(NT2 % NI == 0 || NI % NT2 == 0, "item mapping");
+  constexpr int IPT = NI > NT2 ? NI / NT2 : 1;  // items per thread
+  constexpr int TS = NT2 >= NI ? NT2 / NI : 1;   // token split
+  BinPair acc[IPT][kBcaQMax][kBcaQMax];
+#pragma unroll
+  for (int a = 0; a < IPT; ++a)
+#pragma unroll
+    for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+      for (int j = 0; j < kBcaQMax; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
+    const int nv = ntok * q;
+    const int sb = L::STAGES == 2 ? (it & 1) : 0;
+    const T* st = reinterpret_cast<const T*>(stg + sb * P::STAGE);
+    mbar_wait(gbar + sb, phase_use[sb] & 1);
+    ++phase_use[sb];
+    p2_pass1_fwd<P>(rh, st, nv, k65536);
+    __syncthreads();
+    const int64_t nxt = tile + (int64_t)L::STAGES * gridDim.x;
+    if (lt == 0 && nxt < ntiles)
+      stage_issue(src + nxt * TT * tok_elems, tile_bytes(nxt), stg + sb * P::STAGE, gbar + sb);
+    p2_last_fwd<P>(rh, nv);
+    p2_dc_fwd<P>(rh, nv);
+    __syncthreads();
+    // ---- products: Acc += conj(X) G ; D = sum_i conj(W_ij) G_i written over X
+#pragma unroll
+    for (int a = 0; a < IPT; ++a) {
+      const int u = (tid % NI) + a * NT2;
+      const int ts = NT2 >= NI ? tid / NI : 0;
+      int oa, ob;
+      bca_item_offsets<P>(u, oa, ob);
+      const bool special = (u == 0);
+      BinPair wv[kBcaQMax][kBcaQMax];
+#pragma unroll
+      for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+        for (int j = 0; j < kBcaQMax; ++j)
+          if (i < q && j < q) wv[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
+      for (int tt = ts; tt < ntok; tt += TS) {
+        BinPair xv[kBcaQMax], gv[kBcaQMax];
+#pragma unroll
+        for (int j = 0; j < kBcaQMax; ++j)
+          if (j < q) {
+            xv[j] = bins_get(Hx + P::row(tt * q + j), oa, ob, special);
+            gv[j] = bins_get(Hg + P::row(tt * q + j), oa, ob, special);
+          }
+#pragma unroll
+        for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+          for (int j = 0; j < kBcaQMax; ++j)
+            if (i < q && j < q) {
+              acc[a][i][j].b1 = special ? rfma(xv[j].b1, gv[i].b1, acc[a][i][j].b1)
+                                        : cfmac(xv[j].b1, gv[i].b1, acc[a][i][j].b1);
+              acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
+            }
+#pragma unroll
+        for (int j = 0; j < kBcaQMax; ++j) {
+          if (j < q) {
+            BinPair d = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+            for (int i = 0; i < kBcaQMax; ++i)
+              if (i < q) {
+                d.b1 = special ? rfma(wv[i][j].b1, gv[i].b1, d.b1) : cfmac(wv[i][j].b1, gv[i].b1, d.b1);
+                d.b2 = cfmac(wv[i][j].b2, gv[i].b2, d.b2);
+              }
+            bins_put(Hx + P::row(tt * q + j), oa, ob, special, d);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- dx = IrdFFT(D): group 0 (the x group owns Hx)
+    if (grp == 0) {
+      p2_last_inv<P>(rh, nv);
+      p2_dc_inv<P>(rh, nv);
+    }
+    __syncthreads();
+    if (grp == 0) p2_pass1_inv<P>(rh, dx + tile * TT * tok_elems, nv);
+    __syncthreads();
+  }
+  // ---- flush dW accumulators (packed slots) into dw with fp32 atomics
+#pragma unroll
+  for (int a = 0; a < IPT; ++a) {
+    const int u = (tid % NI) + a * NT2;
+    const int ts = NT2 >= NI ? tid / NI : 0;
+    (void)ts;
+#pragma unroll
+    for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+      for (int j = 0; j < kBcaQMax; ++j) {
+        if (i < q && j < q) {
+          float* d = dw + (int64_t)(i * q + j) * N;
+          const BinPair v = acc[a][i][j];
+          if (u == 0) {
+            atomicAdd(d + 0, v.b1.x);
+            atomicAdd(d + N / 2, v.b1.y);
+            atomicAdd(d + N / 4, v.b2.x);
+            atomicAdd(d + 3 * N / 4, v.b2.y);
+          } else {
+            atomicAdd(d + u, v.b1.x);
+            atomicAdd(d + N - u, v.b1.y);
+            atomicAdd(d + N / 2 - u, v.b2.x);
+            atomicAdd(d + N / 2 + u, v.b2.y);
+          }
+        }
+      }
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+template <typename P, typename K>
+int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (per_sm <= 0) return 0;
+  return (int)(units < (int64_t)per_sm * sms ? units : (int64_t)per_sm * sms);
+}
+
+template <typename P>
+bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int q,
+                     int sms, cudaStream_t st) {
+  using L = BcaFwdSmem<P>;
+  auto k = bca_fwd2_kernel<P>;
+  const int TT = P::VT / q;
+  const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
+  if (grid <= 0) return false;
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_, q);
+  return true;
+}
+
+template <typename P>
+bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
+                     typename P::elem* dx, float* dw, int64_t T_, int q, int sms, cudaStream_t st) {
+  using L = BcaBwdSmem<P>;
+  auto k = bca_bwd2_kernel<P>;
+  const int TT = P::VT / q;
+  const int grid = bca2_grid<P>(k, 2 * P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
+  if (grid <= 0) return false;
+  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, q);
+  return true;
+}
+
+// Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
+template <typename T>
+bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
+  if (q_in != q_out || q_in > kBcaQMax) return false;
+  switch (p) {
+    case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16>>(x, w, y, T_, q_in, sms, st);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16>>(x, w, y, T_, q_in, sms, st);
+    case 1024: return launch_bca_fwd2<Plan2<T, 1024, 32, 16>>(x, w, y, T_, q_in, sms, st);
+    default: return false;
+  }
+}
+
+template <typename T>
+bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
+                  int sms, cudaStream_t st) {
+  if (q_in != q_out || q_in > kBcaQMax) return false;
+  switch (p) {
+    case 256: return launch_bca_bwd2<Plan2<T, 256, 16, 16>>(x, w, g, dx, dw, T_, q_in, sms, st);
+    case 512: return launch_bca_bwd2<Plan2<T, 512, 32, 8>>(x, w, g, dx, dw, T_, q_in, sms, st);
+    case 1024: return launch_bca_bwd2<Plan2<T, 1024, 32, 8>>(x, w, g, dx, dw, T_, q_in, sms, st);
+    default: return false;
+  }
+}
+
+}  // namespace rdfft
