@@ -1,6 +1,6 @@
 #!/bin/bash
 # Run on the GPU box (via gpurun): bench line, ncu launch list of one bench step, and one
-# `ncu --set full` capture per hot kernel.  Outputs under gpurun_out/$TAG/.
+# `ncu --set full` capture per hot kernel of the bench step.  Outputs under gpurun_out/$TAG/.
 set -x
 TAG=${1:-run}
 OUT=gpurun_out/$TAG
@@ -9,8 +9,10 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.draw --form
 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $OUT/launches_bench.log 2>&1
-for K in rdfft_fwd2 rdfft_inv2 packed_mul bca_fwd bca_bwd; do
-  ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -o $OUT/prof_$K \
-      python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --batch 262144 > $OUT/ncu_$K.log 2>&1
+i=0
+for K in "rdfft2_kernel.*bfloat16.*false" "rdfft2_kernel.*bfloat16.*true" "packed_mul" "bca_fwd" "bca_bwd"; do
+  i=$((i+1))
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K" -s 1 -c 1 \
+      -o $OUT/prof_$i python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --batch 262144 > $OUT/ncu_$i.log 2>&1
 done
 ls -la $OUT
