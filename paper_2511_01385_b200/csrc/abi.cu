@@ -11,6 +11,7 @@
 #include "bca_v1.cuh"
 #include "kernels_v1.cuh"
 #include "plan2.cuh"
+#include "plan3.cuh"
 #include "bca2.cuh"
 
 using namespace rdfft;

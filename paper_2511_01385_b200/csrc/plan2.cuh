@@ -467,17 +467,4 @@ bool launch_plan2(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
   return true;
 }
 
-// Returns true when a specialised kernel was launched for (n, T).
-template <typename T>
-bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st) {
-  (void)logn;
-  switch (n) {
-    case 128: return launch_plan2<Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
-    case 256: return launch_plan2<Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
-    case 512: return launch_plan2<Plan2<T, 512, 32, 8>>(x, batch, inverse, sms, st);
-    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8>>(x, batch, inverse, sms, st);
-    default: return false;
-  }
-}
-
 }  // namespace rdfft

@@ -1,0 +1,420 @@
+// plan3.cuh — three-pass register-blocked rdFFT for n = 2048, 4096 (sm_100a).
+//
+// n = R * M2 * M3 with R = 32 (pass 1, the paper's first 5 stages per decimated
+// subsequence, exactly as plan2), M2 = 4 (middle pass: stages m = 32, 64 on the
+// closed sets S_k = {j 32 +- k} of each 128-slot window, both half-pair windows
+// in the two float2 lanes), M3 = n / 128 (last pass: stages m = 128 .. n/2 on
+// S_k = {j 128 +- k}, k = 1 .. 64).  Every pass is the paper's radix-2 stages
+// regrouped as "twiddle + small complex DIT FFT" on a Prop. 1 closed set; the
+// block DCs of each pass form a real FFT run by dedicated lanes.  The shared
+// layout (padded 32-slot windows, half pairs, row skew) is plan2's.
+#pragma once
+
+#include "plan2.cuh"
+
+namespace rdfft {
+
+template <typename T, int N_, int VT_>
+struct Plan3 {
+  using elem = T;
+  static constexpr int N = N_, VT = VT_, R = 32;
+  static constexpr int M2 = 4, W2 = 128;     // middle pass
+  static constexpr int M3 = N / W2, LM3 = ilog2c<M3>();
+  static constexpr int LR = 5, S = N / R, LS = ilog2c<S>(), P1 = S / 2;
+  static constexpr int NT = VT * P1;
+  static constexpr int WSTR = R + 2;
+  static constexpr int NWIN = S / 2;
+  static constexpr int ROWA = ((NWIN * WSTR + 14 + 15) / 16) * 16;
+  static constexpr int HF = VT * ROWA + 16;
+  static constexpr int KM = R / 2;           // middle-pass lanes per window (k = 1 .. 16)
+  static constexpr int WPV = N / (2 * W2);   // middle-pass windows per vector (first half)
+  static constexpr int MIPV = WPV * KM;      // middle general items per vector
+  static constexpr int KL = W2 / 2;          // last-pass lanes per vector (k = 1 .. 64)
+  static constexpr int TWM = M2 * KM, TWL = M3 * KL;
+  static constexpr int CHV = N / 4;
+  static constexpr int STAGE = VT * N * (int)sizeof(T);
+  static_assert(M3 >= 4 && M3 <= 32, "plan3 shape");
+  static_assert(NT % 32 == 0 && NT % MIPV == 0 && (VT * KL) % NT == 0 && CHV % NT == 0, "plan3 mapping");
+  static_assert(VT <= 8, "compile-time skew offsets assume v < 8");
+  __host__ __device__ static constexpr int skew(int v) { return 2 * (v & 7); }
+  __host__ __device__ static constexpr int row(int v) { return v * ROWA + skew(v); }
+  // physical float2 offset (within a row) of logical half-pair index q
+  __host__ __device__ static constexpr int pos(int q) { return (q / R) * WSTR + (q % R); }
+};
+
+template <typename P>
+struct P3Smem {  // [stage 0][stage 1][H][TWm][TWl][bars]
+  static constexpr size_t H_OFF = 2 * (size_t)P::STAGE;
+  static constexpr size_t TWM_OFF = H_OFF + (size_t)P::HF * 8;
+  static constexpr size_t TWL_OFF = TWM_OFF + (size_t)P::TWM * 8;
+  static constexpr size_t BAR_OFF = TWL_OFF + (size_t)P::TWL * 8;
+  static constexpr size_t BYTES = BAR_OFF + 16;
+};
+
+// Middle-pass general set on both half-pair lanes: Z_j(k), j < 4, of one 128-slot window.
+template <bool kInv>
+__device__ __forceinline__ void p3_mid_set(float2* ha, float2* hm, const float2* hmi, float2* hmo, const float2* tw) {
+  constexpr int M = 4, WS = 34;
+  float zr[2][M], zi[2][M];
+  if (!kInv) {
+    ct::static_for<0, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      const float2 a = ha[j * WS], b = hmi[j * WS];
+      zr[0][j] = a.x; zr[1][j] = a.y;
+      zi[0][j] = b.x; zi[1][j] = b.y;
+    });
+    ct::static_for<1, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      const float2 t = tw[j * 16];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float q = zr[h][j];
+        zr[h][j] = fmaf(q, t.x, -zi[h][j] * t.y);
+        zi[h][j] = fmaf(q, t.y, zi[h][j] * t.x);
+      }
+    });
+    cfft_dit<M>(zr[0], zi[0]);
+    cfft_dit<M>(zr[1], zi[1]);
+    // asc[q] <- q < 2 ? Re Y[q] : -Im Y[q];  mirror[3 - q] <- q < 2 ? Im Y[q] : Re Y[q]
+    ct::static_for<0, M>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      if constexpr (q < M / 2) {
+        ha[q * WS] = make_float2(zr[0][q], zr[1][q]);
+        hm[(M - 1 - q) * WS] = make_float2(zi[0][q], zi[1][q]);
+      } else {
+        ha[q * WS] = make_float2(-zi[0][q], -zi[1][q]);
+        hm[(M - 1 - q) * WS] = make_float2(zr[0][q], zr[1][q]);
+      }
+    });
+  } else {
+    // Y[q] from the packed window; load into register rev(q) for the conjugate DIT pass
+    ct::static_for<0, M>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      constexpr int rq = rev_bits<2>(q);
+      const float2 a = ha[q * WS], b = hm[(M - 1 - q) * WS];
+      if constexpr (q < M / 2) {
+        zr[0][rq] = a.x; zr[1][rq] = a.y;
+        zi[0][rq] = b.x; zi[1][rq] = b.y;
+      } else {
+        zi[0][rq] = -a.x; zi[1][rq] = -a.y;
+        zr[0][rq] = b.x; zr[1][rq] = b.y;
+      }
+    });
+    cfft_dit<M, true>(zr[0], zi[0]);
+    cfft_dit<M, true>(zr[1], zi[1]);
+    ct::static_for<0, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int rj = rev_bits<2>(j);
+      if constexpr (j > 0) {
+        const float2 t = tw[j * 16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float q = zr[h][rj];
+          zr[h][rj] = fmaf(q, t.x, -zi[h][rj] * t.y);
+          zi[h][rj] = fmaf(q, t.y, zi[h][rj] * t.x);
+        }
+      }
+      ha[j * WS] = make_float2(zr[0][rj], zr[1][rj]);
+      hmo[j * WS] = make_float2(zi[0][rj], zi[1][rj]);
+    });
+  }
+}
+
+// Last-pass general set: S_k = {j 128 +- k}, M3 blocks, half pairs hold (Z_j, Z_{j + M3/2}).
+template <int M, bool kInv>
+__device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2* hmi, float2* hmo, const float2* tw) {
+  constexpr int WS = 4 * 34, LM = ilog2c<M>();  // 128 slots = 4 padded windows
+  float zr[M], zi[M];
+  if (!kInv) {
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      const float2 a = ha[jj * WS], b = hmi[jj * WS];
+      zr[jj] = a.x; zr[jj + M / 2] = a.y;
+      zi[jj] = b.x; zi[jj + M / 2] = b.y;
+    });
+    ct::static_for<1, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      const float2 t = tw[j * 64];
+      const float q = zr[j];
+      zr[j] = fmaf(q, t.x, -zi[j] * t.y);
+      zi[j] = fmaf(q, t.y, zi[j] * t.x);
+    });
+    cfft_dit<M>(zr, zi);
+    ct::static_for<0, M / 2>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      ha[q * WS] = make_float2(zr[q], -zi[q + M / 2]);
+      hm[(M / 2 - 1 - q) * WS] = make_float2(zr[q + M / 2], zi[q]);
+    });
+  } else {
+    ct::static_for<0, M / 2>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      const float2 a = ha[q * WS], b = hm[(M / 2 - 1 - q) * WS];
+      zr[rev_bits<LM>(q)] = a.x;
+      zi[rev_bits<LM>(q + M / 2)] = -a.y;
+      zr[rev_bits<LM>(q + M / 2)] = b.x;
+      zi[rev_bits<LM>(q)] = b.y;
+    });
+    cfft_dit<M, true>(zr, zi);
+    ct::static_for<0, M>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      constexpr int rj = rev_bits<LM>(j);
+      const float2 t = tw[j * 64];
+      const float q = zr[rj];
+      zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
+      zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
+    });
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      constexpr int r1 = rev_bits<LM>(jj), r2 = rev_bits<LM>(jj + M / 2);
+      ha[jj * WS] = make_float2(zr[r1], zr[r2]);
+      hmo[jj * WS] = make_float2(zi[r1], zi[r2]);
+    });
+  }
+}
+
+// DC set of a pass: M reals-pairs at stride WS (float2 lanes), real M-point FFT (unscaled inverse).
+template <int M, int WS, bool kInv, typename V>
+__device__ __forceinline__ void p3_dc_set(float2* hd, float scale) {
+  V d[M];
+  ct::static_for<0, (sizeof(V) == 8 ? M : M / 2)>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    if constexpr (sizeof(V) == 8) {
+      d[j] = *reinterpret_cast<V*>(hd + j * WS);
+    } else {  // scalar lanes: (D_j, D_{j + M/2}) in one half pair
+      const float2 a = hd[j * WS];
+      reinterpret_cast<float*>(d)[j] = a.x;
+      reinterpret_cast<float*>(d)[j + M / 2] = a.y;
+    }
+  });
+  if (!kInv)
+    rfft_fwd_reg<M>(d);
+  else
+    rfft_inv_reg<M>(d);
+  ct::static_for<0, (sizeof(V) == 8 ? M : M / 2)>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    if constexpr (sizeof(V) == 8) {
+      const float2 v = *reinterpret_cast<float2*>(&d[j]);
+      hd[j * WS] = make_float2(v.x * scale, v.y * scale);
+    } else {
+      hd[j * WS] = make_float2(reinterpret_cast<float*>(d)[j] * scale, reinterpret_cast<float*>(d)[j + M / 2] * scale);
+    }
+  });
+}
+
+template <typename P, bool kInv>
+__global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restrict__ x, int64_t batch) {
+  using T = typename P::elem;
+  using L = P3Smem<P>;
+  constexpr int VT = P::VT, N = P::N, NT = P::NT, R = P::R, S = P::S, WS = P::WSTR;
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  float2* H = reinterpret_cast<float2*>(base + L::H_OFF);
+  float2* TWm = reinterpret_cast<float2*>(base + L::TWM_OFF);
+  float2* TWl = reinterpret_cast<float2*>(base + L::TWL_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
+  const int tid = threadIdx.x;
+  // tables: TWm[j 16 + k-1] = W_128^{k rev2(j)}, TWl[j 64 + k-1] = W_N^{k rev(j)}; inverse: conj (and 1/N on TWl)
+  for (int e = tid; e < P::TWM; e += NT) {
+    const int j = e / 16, k = 1 + e % 16;
+    float s, c;
+    sincospif(2.0f * (float)(k * rev_bits<2>(j)) / 128.0f, &s, &c);
+    TWm[e] = kInv ? make_float2(c, s) : make_float2(c, -s);
+  }
+  for (int e = tid; e < P::TWL; e += NT) {
+    const int j = e / 64, k = 1 + e % 64;
+    float s, c;
+    sincospif(2.0f * (float)(k * rev_bits<P::LM3>(j)) / (float)N, &s, &c);
+    TWl[e] = kInv ? make_float2(c * (1.0f / N), s * (1.0f / N)) : make_float2(c, -s);
+  }
+  for (int e = tid; e < P::NWIN * VT; e += NT) {  // window pads (zero imaginary inputs)
+    float2* pad = H + P::row(e / P::NWIN) + (e % P::NWIN) * WS + R;
+    pad[0] = make_float2(0.f, 0.f);
+    pad[1] = make_float2(0.f, 0.f);
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  // ---- roles
+  const int v1 = tid / P::P1, w1 = tid % P::P1;
+  const int c1 = rev_bits<P::LS - 1>(w1);
+  float2* h1 = H + P::row(v1) + w1 * WS;
+  const int s1 = v1 * N + 2 * c1;
+  // middle general: item it = tid + NT r -> vector vm(r), window wm, k km (tid-part fixed)
+  const int mrem = tid % P::MIPV;
+  const int vm0 = tid / P::MIPV;
+  const int wm = mrem / P::KM, km = 1 + mrem % P::KM;
+  float2* mha = H + P::row(vm0) + 4 * wm * WS + km;
+  float2* mhm = H + P::row(vm0) + 4 * wm * WS + (R - km);
+  float2* mhz = (km == R / 2) ? (H + P::row(vm0) + 4 * wm * WS + R) : mhm;  // pad: zero input / sink
+  const float2* mtw = TWm + (km - 1);
+  constexpr int MSTEP = NT / P::MIPV;  // vectors advanced per item step
+  constexpr int MITEMS = VT * P::MIPV / NT;
+  // middle DC items: (vector, window), VT * WPV of them, on the last threads
+  constexpr int NDCM = VT * P::WPV;
+  const int dcm = tid - (NT - NDCM);
+  float2* mhd = H + P::row(dcm < 0 ? 0 : dcm / P::WPV) + 4 * ((dcm < 0 ? 0 : dcm) % P::WPV) * WS;
+  // last general: item it = tid + NT r -> vector vl0 + r LSTEP, k kl
+  const int vl0 = tid / P::KL, kl = 1 + tid % P::KL;
+  const int qa = kl, qm = P::W2 - kl;
+  float2* lha = H + P::row(vl0) + P::pos(qa);
+  float2* lhm = H + P::row(vl0) + P::pos(qm);
+  float2* lhz = (kl == P::KL) ? (H + P::row(vl0) + P::pos(qa) + (R - (qa % R))) : lhm;
+  const float2* ltw = TWl + (kl - 1);
+  constexpr int LSTEP = NT / P::KL;
+  constexpr int LITEMS = VT * P::KL / NT;
+  const int dcl = tid - (NT - VT);  // last DC: one lane per vector on the last threads
+  float2* lhd = H + P::row(dcl < 0 ? 0 : dcl);
+  // chunks
+  float2* hq = H + (2 * tid / R) * WS + (2 * tid) % R;
+  const uint32_t k65536 = kTwo16;
+  const int64_t ntiles = (batch + VT - 1) / VT;
+  auto tile_bytes = [&](int64_t t) {
+    const int64_t nv = batch - t * VT < VT ? batch - t * VT : VT;
+    return (uint32_t)(nv * N * (int)sizeof(T));
+  };
+  __syncthreads();
+  if (tid == 0) {
+    for (int q = 0; q < 2; ++q) {
+      const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
+      if (t < ntiles) stage_issue(x + t * VT * (int64_t)N, tile_bytes(t), base + q * P::STAGE, bar + q);
+    }
+  }
+  auto middle = [&](int nv) {
+    ct::static_for<0, MITEMS>([&](auto RR) {
+      constexpr int r = decltype(RR)::value;
+      constexpr int dv = r * MSTEP;
+      constexpr int off = dv * P::ROWA + 2 * dv;  // row(vm0 + dv) - row(vm0), v < 8
+      if (vm0 + dv < nv) p3_mid_set<kInv>(mha + off, mhm + off, mhz + off, mhz + off, mtw);
+    });
+    if (dcm >= 0 && dcm / P::WPV < nv) p3_dc_set<4, WS, kInv, float2>(mhd, 1.0f);
+  };
+  auto last = [&](int nv) {
+    ct::static_for<0, LITEMS>([&](auto RR) {
+      constexpr int r = decltype(RR)::value;
+      constexpr int dv = r * LSTEP;
+      constexpr int off = dv * P::ROWA + 2 * dv;
+      if (vl0 + dv < nv) p3_last_set<P::M3, kInv>(lha + off, lhm + off, lhz + off, lhz + off, ltw);
+    });
+    if (dcl >= 0 && dcl < nv) p3_dc_set<P::M3, 4 * WS, kInv, float>(lhd, kInv ? 1.0f / N : 1.0f);
+  };
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
+    T* xt = x + tile * VT * (int64_t)N;
+    const int sb = it & 1;
+    const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
+    const int64_t nxt = tile + 2 * (int64_t)gridDim.x;
+    mbar_wait(bar + sb, (it >> 1) & 1);
+    if (!kInv) {
+      if (v1 < nv) {  // pass 1 (plan2's)
+        float2 b[R];
+        const T* src = st + s1;
+        ct::static_for<0, R>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          b[rev_bits<P::LR>(i)] = sio<T>::ld2(src + S * i, k65536);
+        });
+        rfft_fwd_reg<R>(b);
+        ct::static_for<0, R / 2>([&](auto I) {
+          constexpr int i = 2 * decltype(I)::value;
+          *reinterpret_cast<float4*>(h1 + i) = make_float4(b[i].x, b[i].y, b[i + 1].x, b[i + 1].y);
+        });
+      }
+      __syncthreads();
+      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+      middle(nv);
+      __syncthreads();
+      last(nv);
+      __syncthreads();
+      ct::static_for<0, VT * P::CHV / NT>([&](auto RR) {  // store
+        constexpr int r = decltype(RR)::value;
+        constexpr int v = r / (P::CHV / NT), toff = NT * (r % (P::CHV / NT));
+        if (v < nv) {
+          const float4 f = *reinterpret_cast<const float4*>(hq + P::row(v) + (2 * toff / R) * WS);
+          T* d = xt + v * N + 2 * (tid + toff);
+          gio<T>::st2(d, make_float2(f.x, f.z));
+          gio<T>::st2(d + N / 2, make_float2(f.y, f.w));
+        }
+      });
+    } else {
+      ct::static_for<0, VT * P::CHV / NT>([&](auto RR) {  // load
+        constexpr int r = decltype(RR)::value;
+        constexpr int v = r / (P::CHV / NT), toff = NT * (r % (P::CHV / NT));
+        if (v < nv) {
+          const T* s = st + v * N + 2 * (tid + toff);
+          const float2 lo = sio<T>::ld2(s, k65536), hi = sio<T>::ld2(s + N / 2, k65536);
+          *reinterpret_cast<float4*>(hq + P::row(v) + (2 * toff / R) * WS) = make_float4(lo.x, hi.x, lo.y, hi.y);
+        }
+      });
+      __syncthreads();
+      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+      last(nv);
+      __syncthreads();
+      middle(nv);
+      __syncthreads();
+      if (v1 < nv) {  // inverse pass 1
+        float2 b[R];
+        ct::static_for<0, R / 2>([&](auto I) {
+          constexpr int i = 2 * decltype(I)::value;
+          const float4 f = *reinterpret_cast<const float4*>(h1 + i);
+          b[i] = make_float2(f.x, f.y);
+          b[i + 1] = make_float2(f.z, f.w);
+        });
+        rfft_inv_reg<R>(b);
+        T* dst = xt + s1;
+        ct::static_for<0, R>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          gio<T>::st2(dst + S * i, b[rev_bits<P::LR>(i)]);
+        });
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename P>
+bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
+  using L = P3Smem<P>;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
+  auto kf = rdfft3_kernel<P, false>;
+  auto ki = rdfft3_kernel<P, true>;
+  static bool configured = false;
+  static int per_sm = 1;
+  if (!configured) {
+    for (auto k : {kf, ki}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    }
+    int a = 0, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kf, P::NT, L::BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ki, P::NT, L::BYTES);
+    per_sm = a < b ? a : b;
+    if (per_sm < 1) per_sm = 1;
+    configured = true;
+  }
+  const int64_t tiles = (batch + P::VT - 1) / P::VT;
+  const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
+  if (inverse)
+    ki<<<grid, P::NT, L::BYTES, st>>>(x, batch);
+  else
+    kf<<<grid, P::NT, L::BYTES, st>>>(x, batch);
+  return true;
+}
+
+// Returns true when a specialised kernel was launched for (n, T).
+template <typename T>
+bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st) {
+  (void)logn;
+  switch (n) {
+    case 128: return launch_plan2<Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
+    case 256: return launch_plan2<Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
+    case 512: return launch_plan2<Plan2<T, 512, 32, 8>>(x, batch, inverse, sms, st);
+    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8>>(x, batch, inverse, sms, st);
+    case 2048: return launch_plan3<Plan3<T, 2048, 4>>(x, batch, inverse, sms, st);
+    case 4096: return launch_plan3<Plan3<T, 4096, 4>>(x, batch, inverse, sms, st);
+    default: return false;
+  }
+}
+
+}  // namespace rdfft
