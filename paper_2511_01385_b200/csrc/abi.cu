@@ -88,6 +88,31 @@ int packed(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, in
   if (overlap(a, batch * n * s, b, b_batch * n * s) && !(a == b && b_batch == batch)) return RDFFT_E_ALIAS;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logn = ilog2(n);
+  if (n >= 16 && aligned16(a) && aligned16(b)) {
+    const int rows = (kPm2TileBytes / (int)s) >> logn;
+    const int64_t tiles = (batch + rows - 1) / rows;
+    const size_t smem = (size_t)kPm2Stages * kPm2TileBytes +
+                        (b_batch == 1 ? ((n * s + 15) & ~(size_t)15) : (size_t)kPm2Stages * kPm2TileBytes) +
+                        (2 * kPm2Stages + 1) * 8;
+    if (dtype == RDFFT_F32) {
+      for (auto k : {packed_mul2_kernel<float, false>, packed_mul2_kernel<float, true>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    } else {
+      for (auto k : {packed_mul2_kernel<__nv_bfloat16, false>, packed_mul2_kernel<__nv_bfloat16, true>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    }
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (smem + 1024)));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * per_sm));
+#define RDFFT_PM2(T, C) \
+  packed_mul2_kernel<T, C><<<grid, kPm2Threads, smem, st>>>(static_cast<T*>(a), static_cast<const T*>(b), batch, (int)n, logn, b_batch)
+    if (dtype == RDFFT_F32) {
+      if (conj) RDFFT_PM2(float, true); else RDFFT_PM2(float, false);
+    } else {
+      if (conj) RDFFT_PM2(__nv_bfloat16, true); else RDFFT_PM2(__nv_bfloat16, false);
+    }
+#undef RDFFT_PM2
+    return launched();
+  }
   const int rows = (kPmTileBytes / (int)s) >> logn;
   const int64_t tiles = (batch + rows - 1) / rows;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * 6));
