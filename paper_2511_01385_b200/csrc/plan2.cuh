@@ -70,10 +70,11 @@ struct gio<__nv_bfloat16> {
   }
 };
 
-template <typename T, int N_, int R_, int VT_>
+template <typename T, int N_, int R_, int VT_, int NSTG_ = 2>
 struct Plan2 {
   using elem = T;
   static constexpr int N = N_, R = R_, VT = VT_;
+  static constexpr int NSTG = NSTG_;  // staging buffers (TMA ring depth) of the stand-alone transforms
   static constexpr int LN = ilog2c<N>();
   static constexpr int LR = ilog2c<R>();
   static constexpr int M = N / R;           // last-pass FFT size (blocks per vector)
@@ -370,11 +371,11 @@ __device__ __forceinline__ void stage_issue(const T* src, uint32_t bytes, void* 
 
 // ---------------------------------------------------------------- rdfft kernels
 template <typename P>
-struct P2Smem {  // [stage 0][stage 1][H][TW][bars]
-  static constexpr size_t H_OFF = 2 * (size_t)P::STAGE;
+struct P2Smem {  // [stage 0 .. NSTG-1][H][TW][bars]
+  static constexpr size_t H_OFF = (size_t)P::NSTG * P::STAGE;
   static constexpr size_t TW_OFF = H_OFF + (size_t)P::HF * 8;
   static constexpr size_t BAR_OFF = TW_OFF + (size_t)P::TWF * 8;
-  static constexpr size_t BYTES = BAR_OFF + 16;
+  static constexpr size_t BYTES = BAR_OFF + 8 * P::NSTG;
 };
 
 template <typename P, bool kInv>
@@ -391,8 +392,7 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   p2_tables<P>(kInv ? nullptr : TW, kInv ? TW : nullptr, tid, P::NT);
   if (!kInv) p2_zero_pads<P>(H, VT, tid, P::NT);
   if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    for (int q = 0; q < P::NSTG; ++q) mbar_init(bar + q, 1);
     fence_mbar_init();
   }
   const P2Roles<P> r(H, TW, TW, tid);
@@ -403,8 +403,9 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
     return (uint32_t)(nv * N * (int)sizeof(T));
   };
   __syncthreads();
+  constexpr int NS = P::NSTG;
   if (tid == 0) {
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NS; ++q) {
       const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
       if (t < ntiles) stage_issue(x + t * VT * (int64_t)N, tile_bytes(t), base + q * P::STAGE, bar + q);
     }
@@ -413,10 +414,10 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
     T* xt = x + tile * VT * (int64_t)N;
-    const int sb = it & 1;
+    const int sb = it % NS;
     const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
-    const int64_t nxt = tile + 2 * (int64_t)gridDim.x;
-    mbar_wait(bar + sb, (it >> 1) & 1);
+    const int64_t nxt = tile + NS * (int64_t)gridDim.x;
+    mbar_wait(bar + sb, (it / NS) & 1);
     if (!kInv) {
       p2_pass1_fwd<P>(r, st, nv, k65536);
       __syncthreads();  // H complete; staging buffer sb consumed

@@ -409,8 +409,8 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
   switch (n) {
     case 128: return launch_plan2<Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
     case 256: return launch_plan2<Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
-    case 512: return launch_plan2<Plan2<T, 512, 32, 8>>(x, batch, inverse, sms, st);
-    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8>>(x, batch, inverse, sms, st);
+    case 512: return launch_plan2<Plan2<T, 512, 32, 8, 1>>(x, batch, inverse, sms, st);
+    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8, 1>>(x, batch, inverse, sms, st);
     case 2048: return launch_plan3<Plan3<T, 2048, 4>>(x, batch, inverse, sms, st);
     case 4096: return launch_plan3<Plan3<T, 4096, 4>>(x, batch, inverse, sms, st);
     default: return false;
