@@ -285,7 +285,7 @@ def run_gpu(args):
         ach = b / (seg[k] * 1e-3) / 1e9
         rooflines[k] = {"ms": seg[k], "achieved_GBps": ach, "frac": ach / hbm, "bytes": b}
     dom = max(kern_bytes, key=lambda k: seg[k])
-    traffic = ncu_traffic(dom)
+    traffic = ncu_traffic(dom, batch)
     roofline = {"kernel": dom, "bound": "hbm", "achieved": rooflines[dom]["achieved_GBps"], "peak": hbm,
                 "unit": "GB/s", "frac": rooflines[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
                 "bytes_per_launch": kern_bytes[dom], "ms_per_launch": seg[dom]}
@@ -321,13 +321,21 @@ def run_gpu(args):
     return 0
 
 
-def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu summary."""
+def ncu_traffic(kernel, batch):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed `ncu --set full`
+    capture (profiles/ncu_traffic.json, written by tools/ncu_summary.py).  The transform and
+    packed-multiply captures run at a smaller batch; their traffic is scaled to this launch."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(kernel, {}).get("dram_bytes_per_launch")
+        e = d.get(kernel)
+        if not e:
+            return None
+        t = float(e["dram_bytes_per_launch"])
+        if kernel in ("rdfft_fwd", "rdfft_inv", "packed_mul"):
+            t *= batch / float(e.get("batch", 1 << 18))
+        return t
     except Exception:  # noqa: BLE001
         return None
 

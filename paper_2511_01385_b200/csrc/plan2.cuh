@@ -57,13 +57,20 @@ struct sio<__nv_bfloat16> {
 };
 
 template <typename T>
-struct gio;  // global pair stores (streaming)
+struct gio;  // global pair loads / stores (streaming)
 template <>
 struct gio<float> {
+  __device__ __forceinline__ static float2 ld2(const float* p, uint32_t) {
+    return __ldcs(reinterpret_cast<const float2*>(p));
+  }
   __device__ __forceinline__ static void st2(float* p, float2 v) { __stcs(reinterpret_cast<float2*>(p), v); }
 };
 template <>
 struct gio<__nv_bfloat16> {
+  __device__ __forceinline__ static float2 ld2(const __nv_bfloat16* p, uint32_t k65536) {
+    const uint32_t u = __ldcs(reinterpret_cast<const unsigned int*>(p));
+    return make_float2(__uint_as_float(u * k65536), __uint_as_float(u & 0xffff0000u));
+  }
   __device__ __forceinline__ static void st2(__nv_bfloat16* p, float2 v) {
     __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
     __stcs(reinterpret_cast<unsigned int*>(p), *reinterpret_cast<unsigned int*>(&h));
@@ -168,7 +175,7 @@ __device__ __forceinline__ void p2_zero_pads(float2* H, int nvec, int tid, int n
 
 // ---------------------------------------------------------------- forward pieces
 // pass 1 from a staged tile (shared memory, natural order, element type T)
-template <typename P>
+template <typename P, bool kGlobal = false>
 __device__ __forceinline__ void p2_pass1_fwd(const P2Roles<P>& r, const typename P::elem* st, int nv,
                                              uint32_t k65536) {
   using T = typename P::elem;
@@ -178,7 +185,10 @@ __device__ __forceinline__ void p2_pass1_fwd(const P2Roles<P>& r, const typename
     const T* src = st + r.s1;
     ct::static_for<0, R>([&](auto I) {
       constexpr int i = decltype(I)::value;
-      b[rev_bits<P::LR>(i)] = sio<T>::ld2(src + S * i, k65536);
+      if constexpr (kGlobal)
+        b[rev_bits<P::LR>(i)] = gio<T>::ld2(src + S * i, k65536);
+      else
+        b[rev_bits<P::LR>(i)] = sio<T>::ld2(src + S * i, k65536);
     });
     rfft_fwd_reg<R>(b);
     ct::static_for<0, R / 2>([&](auto I) {
@@ -375,7 +385,7 @@ struct P2Smem {  // [stage 0 .. NSTG-1][H][TW][bars]
   static constexpr size_t H_OFF = (size_t)P::NSTG * P::STAGE;
   static constexpr size_t TW_OFF = H_OFF + (size_t)P::HF * 8;
   static constexpr size_t BAR_OFF = TW_OFF + (size_t)P::TWF * 8;
-  static constexpr size_t BYTES = BAR_OFF + 8 * P::NSTG;
+  static constexpr size_t BYTES = BAR_OFF + 8 * (P::NSTG > 0 ? P::NSTG : 1);
 };
 
 template <typename P, bool kInv>
@@ -392,7 +402,7 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   p2_tables<P>(kInv ? nullptr : TW, kInv ? TW : nullptr, tid, P::NT);
   if (!kInv) p2_zero_pads<P>(H, VT, tid, P::NT);
   if (tid == 0) {
-    for (int q = 0; q < P::NSTG; ++q) mbar_init(bar + q, 1);
+    for (int q = 0; q < (P::NSTG > 0 ? P::NSTG : 1); ++q) mbar_init(bar + q, 1);
     fence_mbar_init();
   }
   const P2Roles<P> r(H, TW, TW, tid);
@@ -404,6 +414,7 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   };
   __syncthreads();
   constexpr int NS = P::NSTG;
+  static_assert(!(kInv && NS == 0), "the inverse transform stages its input");
   if (tid == 0) {
     for (int q = 0; q < NS; ++q) {
       const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
@@ -414,58 +425,62 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
     T* xt = x + tile * VT * (int64_t)N;
-    const int sb = it % NS;
-    const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
-    const int64_t nxt = tile + NS * (int64_t)gridDim.x;
-    mbar_wait(bar + sb, (it / NS) & 1);
-    if (!kInv) {
-      p2_pass1_fwd<P>(r, st, nv, k65536);
-      __syncthreads();  // H complete; staging buffer sb consumed
-      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+    if constexpr (NS == 0) {  // forward without staging: pass 1 loads straight from HBM
+      p2_pass1_fwd<P, true>(r, xt, nv, k65536);
+      __syncthreads();
       p2_last_fwd<P>(r, nv);
       p2_dc_fwd<P>(r, nv);
       __syncthreads();
       p2_store<P>(r, xt, nv);
     } else {
-      p2_load<P>(r, st, nv, k65536);
-      __syncthreads();
-      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
-      p2_last_inv<P>(r, nv);
-      p2_dc_inv<P>(r, nv);
-      __syncthreads();
-      p2_pass1_inv<P>(r, xt, nv);
+      const int sb = it % NS;
+      const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
+      const int64_t nxt = tile + NS * (int64_t)gridDim.x;
+      mbar_wait(bar + sb, (it / NS) & 1);
+      if (!kInv) {
+        p2_pass1_fwd<P>(r, st, nv, k65536);
+        __syncthreads();  // H complete; staging buffer sb consumed
+        if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+        p2_last_fwd<P>(r, nv);
+        p2_dc_fwd<P>(r, nv);
+        __syncthreads();
+        p2_store<P>(r, xt, nv);
+      } else {
+        p2_load<P>(r, st, nv, k65536);
+        __syncthreads();
+        if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+        p2_last_inv<P>(r, nv);
+        p2_dc_inv<P>(r, nv);
+        __syncthreads();
+        p2_pass1_inv<P>(r, xt, nv);
+      }
     }
     __syncthreads();  // H free for the next tile
   }
 }
 
-template <typename P>
-bool launch_plan2(typename P::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
+template <typename P, bool kInv>
+bool launch_plan2_dir(typename P::elem* x, int64_t batch, int sms, cudaStream_t st) {
   using L = P2Smem<P>;
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
-  auto kf = rdfft2_kernel<P, false>;
-  auto ki = rdfft2_kernel<P, true>;
-  static bool configured = false;
-  static int per_sm = 1;
-  if (!configured) {
-    for (auto k : {kf, ki}) {
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    }
-    int a = 0, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, kf, P::NT, L::BYTES);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ki, P::NT, L::BYTES);
-    per_sm = a < b ? a : b;
+  auto k = rdfft2_kernel<P, kInv>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NT, L::BYTES);
     if (per_sm < 1) per_sm = 1;
-    configured = true;
   }
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
-  if (inverse)
-    ki<<<grid, P::NT, L::BYTES, st>>>(x, batch);
-  else
-    kf<<<grid, P::NT, L::BYTES, st>>>(x, batch);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, batch);
   return true;
+}
+
+// forward plan PF, inverse plan PI (may differ in staging depth)
+template <typename PF, typename PI>
+bool launch_plan2(typename PF::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
+  return inverse ? launch_plan2_dir<PI, true>(x, batch, sms, st) : launch_plan2_dir<PF, false>(x, batch, sms, st);
 }
 
 }  // namespace rdfft

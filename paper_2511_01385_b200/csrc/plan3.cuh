@@ -14,10 +14,10 @@
 
 namespace rdfft {
 
-template <typename T, int N_, int VT_>
+template <typename T, int N_, int VT_, int NSTG_ = 2>
 struct Plan3 {
   using elem = T;
-  static constexpr int N = N_, VT = VT_, R = 32;
+  static constexpr int N = N_, VT = VT_, R = 32, NSTG = NSTG_;
   static constexpr int M2 = 4, W2 = 128;     // middle pass
   static constexpr int M3 = N / W2, LM3 = ilog2c<M3>();
   static constexpr int LR = 5, S = N / R, LS = ilog2c<S>(), P1 = S / 2;
@@ -34,7 +34,8 @@ struct Plan3 {
   static constexpr int CHV = N / 4;
   static constexpr int STAGE = VT * N * (int)sizeof(T);
   static_assert(M3 >= 4 && M3 <= 32, "plan3 shape");
-  static_assert(NT % 32 == 0 && NT % MIPV == 0 && (VT * KL) % NT == 0 && CHV % NT == 0, "plan3 mapping");
+  static_assert(NT % 32 == 0 && (NT % MIPV == 0 || MIPV % NT == 0) && (VT * KL) % NT == 0 && CHV % NT == 0,
+                "plan3 mapping");
   static_assert(VT <= 8, "compile-time skew offsets assume v < 8");
   __host__ __device__ static constexpr int skew(int v) { return 2 * (v & 7); }
   __host__ __device__ static constexpr int row(int v) { return v * ROWA + skew(v); }
@@ -44,11 +45,11 @@ struct Plan3 {
 
 template <typename P>
 struct P3Smem {  // [stage 0][stage 1][H][TWm][TWl][bars]
-  static constexpr size_t H_OFF = 2 * (size_t)P::STAGE;
+  static constexpr size_t H_OFF = (size_t)P::NSTG * P::STAGE;
   static constexpr size_t TWM_OFF = H_OFF + (size_t)P::HF * 8;
   static constexpr size_t TWL_OFF = TWM_OFF + (size_t)P::TWM * 8;
   static constexpr size_t BAR_OFF = TWL_OFF + (size_t)P::TWL * 8;
-  static constexpr size_t BYTES = BAR_OFF + 16;
+  static constexpr size_t BYTES = BAR_OFF + 8 * P::NSTG;
 };
 
 // Middle-pass general set on both half-pair lanes: Z_j(k), j < 4, of one 128-slot window.
@@ -232,8 +233,7 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
     pad[1] = make_float2(0.f, 0.f);
   }
   if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    for (int q = 0; q < P::NSTG; ++q) mbar_init(bar + q, 1);
     fence_mbar_init();
   }
   // ---- roles
@@ -241,15 +241,14 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
   const int c1 = rev_bits<P::LS - 1>(w1);
   float2* h1 = H + P::row(v1) + w1 * WS;
   const int s1 = v1 * N + 2 * c1;
-  // middle general: item it = tid + NT r -> vector vm(r), window wm, k km (tid-part fixed)
+  // middle general: item it = tid + NT r -> vector vm0 + dv(r), window wm + dw(r), k km (tid-part fixed)
   const int mrem = tid % P::MIPV;
-  const int vm0 = tid / P::MIPV;
+  const int vm0 = NT >= P::MIPV ? tid / P::MIPV : 0;
   const int wm = mrem / P::KM, km = 1 + mrem % P::KM;
   float2* mha = H + P::row(vm0) + 4 * wm * WS + km;
   float2* mhm = H + P::row(vm0) + 4 * wm * WS + (R - km);
   float2* mhz = (km == R / 2) ? (H + P::row(vm0) + 4 * wm * WS + R) : mhm;  // pad: zero input / sink
   const float2* mtw = TWm + (km - 1);
-  constexpr int MSTEP = NT / P::MIPV;  // vectors advanced per item step
   constexpr int MITEMS = VT * P::MIPV / NT;
   // middle DC items: (vector, window), VT * WPV of them, on the last threads
   constexpr int NDCM = VT * P::WPV;
@@ -275,8 +274,9 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
     return (uint32_t)(nv * N * (int)sizeof(T));
   };
   __syncthreads();
+  constexpr int NS = P::NSTG;
   if (tid == 0) {
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < NS; ++q) {
       const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
       if (t < ntiles) stage_issue(x + t * VT * (int64_t)N, tile_bytes(t), base + q * P::STAGE, bar + q);
     }
@@ -284,8 +284,11 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
   auto middle = [&](int nv) {
     ct::static_for<0, MITEMS>([&](auto RR) {
       constexpr int r = decltype(RR)::value;
-      constexpr int dv = r * MSTEP;
-      constexpr int off = dv * P::ROWA + 2 * dv;  // row(vm0 + dv) - row(vm0), v < 8
+      // NT >= MIPV: item step = NT / MIPV vectors;  NT < MIPV: MIPV / NT steps per vector, each
+      // NT / 16 windows further along the same row
+      constexpr int dv = NT >= P::MIPV ? r * (NT / P::MIPV) : r / (P::MIPV / NT);
+      constexpr int dwin = NT >= P::MIPV ? 0 : (r % (P::MIPV / NT)) * (NT / P::KM);
+      constexpr int off = dv * P::ROWA + 2 * dv + dwin * 4 * WS;  // row(vm0 + dv) - row(vm0), v < 8
       if (vm0 + dv < nv) p3_mid_set<kInv>(mha + off, mhm + off, mhz + off, mhz + off, mtw);
     });
     if (dcm >= 0 && dcm / P::WPV < nv) p3_dc_set<4, WS, kInv, float2>(mhd, 1.0f);
@@ -303,10 +306,10 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
     T* xt = x + tile * VT * (int64_t)N;
-    const int sb = it & 1;
+    const int sb = it % NS;
     const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
-    const int64_t nxt = tile + 2 * (int64_t)gridDim.x;
-    mbar_wait(bar + sb, (it >> 1) & 1);
+    const int64_t nxt = tile + NS * (int64_t)gridDim.x;
+    mbar_wait(bar + sb, (it / NS) & 1);
     if (!kInv) {
       if (v1 < nv) {  // pass 1 (plan2's)
         float2 b[R];
@@ -402,17 +405,21 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
   return true;
 }
 
+#ifndef RDFFT_FWD_NSTG
+#define RDFFT_FWD_NSTG 1  // forward staging depth for n = 512 / 1024 (0 = pass 1 straight from HBM)
+#endif
 // Returns true when a specialised kernel was launched for (n, T).
 template <typename T>
 bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st) {
   (void)logn;
   switch (n) {
-    case 128: return launch_plan2<Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
-    case 256: return launch_plan2<Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
-    case 512: return launch_plan2<Plan2<T, 512, 32, 8, 1>>(x, batch, inverse, sms, st);
-    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8, 1>>(x, batch, inverse, sms, st);
-    case 2048: return launch_plan3<Plan3<T, 2048, 4>>(x, batch, inverse, sms, st);
-    case 4096: return launch_plan3<Plan3<T, 4096, 4>>(x, batch, inverse, sms, st);
+    case 64: return launch_plan2<Plan2<T, 64, 16, 32>, Plan2<T, 64, 16, 32>>(x, batch, inverse, sms, st);
+    case 128: return launch_plan2<Plan2<T, 128, 16, 16>, Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
+    case 256: return launch_plan2<Plan2<T, 256, 16, 16>, Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
+    case 512: return launch_plan2<Plan2<T, 512, 32, 8, RDFFT_FWD_NSTG>, Plan2<T, 512, 32, 8, 1>>(x, batch, inverse, sms, st);
+    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8, RDFFT_FWD_NSTG>, Plan2<T, 1024, 32, 8, 1>>(x, batch, inverse, sms, st);
+    case 2048: return launch_plan3<Plan3<T, 2048, 4, 1>>(x, batch, inverse, sms, st);
+    case 4096: return launch_plan3<Plan3<T, 4096, 2, 1>>(x, batch, inverse, sms, st);
     default: return false;
   }
 }

@@ -15,4 +15,9 @@ for K in "rdfft2_kernel.*bfloat16.*bool.0" "rdfft2_kernel.*bfloat16.*bool.1" "pa
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K" -s 1 -c 1 \
       -o $OUT/prof_$i python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --batch 262144 > $OUT/ncu_$i.log 2>&1
 done
-ls -la $OUT
+
+# summarise on the box (gpurun copies back at most 64 MiB): keep the transform captures only
+python tools/ncu_summary.py --reps $OUT/prof_*.ncu-rep --launches $OUT/launches.csv --bench $OUT/bench.json \
+    --out $OUT/summary > /dev/null 2>&1
+rm -f $OUT/prof_3.ncu-rep $OUT/prof_4.ncu-rep $OUT/prof_5.ncu-rep
+du -sh $OUT

@@ -91,6 +91,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--bench")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--batch", type=int, default=1 << 18, help="vectors per transform launch in the captures")
     a = ap.parse_args()
     md = [f"# ncu summary: {os.path.basename(a.out)}\n"]
     traffic = {}
@@ -116,7 +117,8 @@ def main():
             fam = family(d["kernel"])
             t = d.get("dram_read", 0) + d.get("dram_write", 0)
             traffic.setdefault(fam, {"dram_bytes_per_launch": t, "kernel": short(d["kernel"]),
-                                     "duration_s": d.get("duration"), "source": os.path.basename(rep)})
+                                     "duration_s": d.get("duration"), "source": os.path.basename(rep),
+                                     "batch": a.batch})
             md.append(f"| `{short(d['kernel'])}` | {int(d.get('grid', 0))} x {int(d.get('block', 0))} | "
                       f"{int(d.get('regs', 0))} | {d.get('duration', 0) * 1e6:.1f} | {t / 1e6:.1f} | "
                       f"{d.get('dram_pct', 0):.1f} | {d.get('issue_pct', 0):.1f} | {d.get('occupancy_pct', 0):.1f} | "
