@@ -62,7 +62,7 @@ def short(name):
 
 def family(name):
     if "rdfft2_kernel" in name:
-        return "rdfft_inv" if re.search(r",\s*true>", name) else "rdfft_fwd"
+        return "rdfft_inv" if re.search(r",\s*(?:true|\(bool\)1|1)>\s*\(", name) else "rdfft_fwd"
     for k, f in [("bca_fwd", "bca_fwd"), ("bca_bwd", "bca_bwd"), ("packed_mul", "packed_mul"),
                  ("rdfft2_kernel", "rdfft"), ("rdfft_v1", "rdfft_v1")]:
         if k in name:
