@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librdfft.so")
+LIB_PATH = os.environ.get("RDFFT_LIB") or os.path.join(_HERE, "librdfft.so")  # RDFFT_LIB: A/B variants
 
 F32, BF16 = 0, 1
 _DT = {torch.float32: F32, torch.bfloat16: BF16}
