@@ -28,8 +28,8 @@ namespace rdfft {
 constexpr int kBcaQMax = 4;
 
 template <typename P>
-struct BcaFwdSmem {  // [stage x STAGES][H][W][TWf][TWi][bars]
-  static constexpr int STAGES = sizeof(typename P::elem) == 2 ? 2 : 1;
+struct BcaFwdSmem {  // [stage x STAGES][H][W][TWf][TWi][bars]; STAGES = 0: pass 1 reads x from HBM
+  static constexpr int STAGES = P::NSTG;
   static constexpr int WF = kBcaQMax * kBcaQMax * P::ROWA + 16;
   static constexpr size_t H_OFF = (size_t)STAGES * P::STAGE;
   static constexpr size_t W_OFF = H_OFF + (size_t)P::HF * 8;
@@ -37,6 +37,7 @@ struct BcaFwdSmem {  // [stage x STAGES][H][W][TWf][TWi][bars]
   static constexpr size_t TWI_OFF = TWF_OFF + (size_t)P::TWF * 8;
   static constexpr size_t BAR_OFF = TWI_OFF + (size_t)P::TWF * 8;
   static constexpr size_t BYTES = BAR_OFF + 16;
+  static_assert(STAGES <= 2, "staging depth");
 };
 
 // complex helpers on float2 (re, im)
@@ -118,7 +119,7 @@ __device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int
 }
 
 template <typename P>
-__global__ void __launch_bounds__(P::NT) bca_fwd2_kernel(const typename P::elem* __restrict__ x,
+__global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::elem* __restrict__ x,
                                                          const typename P::elem* __restrict__ w,
                                                          typename P::elem* __restrict__ y, int64_t T_, int q) {
   using T = typename P::elem;
@@ -150,11 +151,16 @@ __global__ void __launch_bounds__(P::NT) bca_fwd2_kernel(const typename P::elem*
   };
   __syncthreads();
   // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors, into the resident region
-  if (tid == 0) stage_issue(w, (uint32_t)(q * q * N * (int)sizeof(T)), base, bar);
-  mbar_wait(bar, 0);
+  if constexpr (L::STAGES > 0) {
+    if (tid == 0) stage_issue(w, (uint32_t)(q * q * N * (int)sizeof(T)), base, bar);
+    mbar_wait(bar, 0);
+  }
   {
     const P2Roles<P> rw(Wr, TWf, TWi, tid);
-    p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(base), q * q, k65536);
+    if constexpr (L::STAGES > 0)
+      p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(base), q * q, k65536);
+    else
+      p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
     __syncthreads();
     p2_last_fwd<P>(rw, q * q);
     p2_dc_fwd<P>(rw, q * q);
@@ -171,14 +177,20 @@ __global__ void __launch_bounds__(P::NT) bca_fwd2_kernel(const typename P::elem*
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
     const int nv = ntok * q;
-    const int sb = L::STAGES == 2 ? (it & 1) : 0;
-    const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
-    mbar_wait(bar + sb, phase_use[sb] & 1);
-    ++phase_use[sb];
-    p2_pass1_fwd<P>(rh, st, nv, k65536);
-    __syncthreads();  // H complete, staging sb consumed
-    const int64_t nxt = tile + (int64_t)L::STAGES * gridDim.x;
-    if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * TT * tok_elems, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+    if constexpr (L::STAGES == 0) {
+      p2_pass1_fwd<P, true>(rh, x + tile * TT * tok_elems, nv, k65536);
+      __syncthreads();
+    } else {
+      const int sb = L::STAGES == 2 ? (it & 1) : 0;
+      const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
+      mbar_wait(bar + sb, phase_use[sb] & 1);
+      ++phase_use[sb];
+      p2_pass1_fwd<P>(rh, st, nv, k65536);
+      __syncthreads();  // H complete, staging sb consumed
+      const int64_t nxt = tile + (int64_t)L::STAGES * gridDim.x;
+      if (tid == 0 && nxt < ntiles)
+        stage_issue(x + nxt * TT * tok_elems, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+    }
     p2_last_fwd<P>(rh, nv);
     p2_dc_fwd<P>(rh, nv);
     __syncthreads();
@@ -417,14 +429,20 @@ bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const
   return true;
 }
 
+#ifndef RDFFT_BCA_FWD_VT
+#define RDFFT_BCA_FWD_VT 16   // p = 1024 forward: 32 vectors (8 tokens of q = 4) per tile, 512 threads
+#endif
+#ifndef RDFFT_BCA_FWD_NSTG
+#define RDFFT_BCA_FWD_NSTG 2  // ... with pass 1 reading x straight from HBM (H + W fill shared memory)
+#endif
 // Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
 template <typename T>
 bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
   if (q_in != q_out || q_in > kBcaQMax) return false;
   switch (p) {
-    case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16>>(x, w, y, T_, q_in, sms, st);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16>>(x, w, y, T_, q_in, sms, st);
-    case 1024: return launch_bca_fwd2<Plan2<T, 1024, 32, 16>>(x, w, y, T_, q_in, sms, st);
+    case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>>(x, w, y, T_, q_in, sms, st);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>>(x, w, y, T_, q_in, sms, st);
+    case 1024: return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, RDFFT_BCA_FWD_NSTG>>(x, w, y, T_, q_in, sms, st);
     default: return false;
   }
 }
