@@ -394,7 +394,6 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
   }
 }
 
-// ------------------------------------------------------------------ dispatch
 template <typename P, typename K>
 int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -404,6 +403,168 @@ int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
   if (per_sm <= 0) return 0;
   return (int)(units < (int64_t)per_sm * sms ? units : (int64_t)per_sm * sms);
 }
+
+// ------------------------------------------------------------------ backward, single group
+// One thread group of NT = VT * LPV threads transforms the x tile and then the g tile (pass 1
+// straight from HBM, no staging), so the product and the dx inverse use every thread; a tile is
+// VT / q tokens.  Shared memory: Hx, Hg, W, tables.
+template <typename P>
+struct BcaBwd3Smem {
+  static constexpr int WF = kBcaQMax * kBcaQMax * P::ROWA + 16;
+  static constexpr size_t HX_OFF = 0;
+  static constexpr size_t HG_OFF = HX_OFF + (size_t)P::HF * 8;
+  static constexpr size_t W_OFF = HG_OFF + (size_t)P::HF * 8;
+  static constexpr size_t TWF_OFF = W_OFF + (size_t)WF * 8;
+  static constexpr size_t TWI_OFF = TWF_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BYTES = TWI_OFF + (size_t)P::TWF * 8;
+};
+
+template <typename P>
+__global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::elem* __restrict__ x,
+                                                            const typename P::elem* __restrict__ w,
+                                                            const typename P::elem* g, typename P::elem* dx,
+                                                            float* __restrict__ dw, int64_t T_, int q) {
+  using T = typename P::elem;
+  using L = BcaBwd3Smem<P>;
+  constexpr int N = P::N, NT = P::NT, NI = N / 4;
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  float2* Hx = reinterpret_cast<float2*>(base + L::HX_OFF);
+  float2* Hg = reinterpret_cast<float2*>(base + L::HG_OFF);
+  float2* Wr = reinterpret_cast<float2*>(base + L::W_OFF);
+  float2* TWf = reinterpret_cast<float2*>(base + L::TWF_OFF);
+  float2* TWi = reinterpret_cast<float2*>(base + L::TWI_OFF);
+  const int tid = threadIdx.x;
+  const int TT = P::VT / q;
+  const int64_t ntiles = (T_ + TT - 1) / TT;
+  const int64_t tok_elems = (int64_t)q * N;
+  p2_tables<P>(TWf, TWi, tid, NT);
+  p2_zero_pads<P>(Hx, P::VT, tid, NT);
+  p2_zero_pads<P>(Hg, P::VT, tid, NT);
+  p2_zero_pads<P>(Wr, q * q, tid, NT);
+  const uint32_t k65536 = kTwo16;
+  const P2Roles<P> rx(Hx, TWf, TWi, tid), rg(Hg, TWf, TWi, tid);
+  __syncthreads();
+  {  // W_ij = rdFFT(w_ij): q*q <= VT vectors
+    const P2Roles<P> rw(Wr, TWf, TWi, tid);
+    p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
+    __syncthreads();
+    p2_last_fwd<P>(rw, q * q);
+    p2_dc_fwd<P>(rw, q * q);
+  }
+  __syncthreads();
+  static_assert(NT % NI == 0 || NI % NT == 0, "item mapping");
+  constexpr int IPT = NI > NT ? NI / NT : 1;  // items per thread
+  constexpr int TS = NT >= NI ? NT / NI : 1;   // token split
+  BinPair acc[IPT][kBcaQMax][kBcaQMax];
+#pragma unroll
+  for (int a = 0; a < IPT; ++a)
+#pragma unroll
+    for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+      for (int j = 0; j < kBcaQMax; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
+    const int nv = ntok * q;
+    p2_pass1_fwd<P, true>(rx, x + tile * TT * tok_elems, nv, k65536);
+    p2_pass1_fwd<P, true>(rg, g + tile * TT * tok_elems, nv, k65536);
+    __syncthreads();
+    p2_last_fwd<P>(rx, nv);
+    p2_last_fwd<P>(rg, nv);
+    p2_dc_fwd<P>(rx, nv);
+    p2_dc_fwd<P>(rg, nv);
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < IPT; ++a) {
+      const int u = (tid % NI) + a * NT;
+      const int ts = NT >= NI ? tid / NI : 0;
+      int oa, ob;
+      bca_item_offsets<P>(u, oa, ob);
+      const bool special = (u == 0);
+      BinPair wv[kBcaQMax][kBcaQMax];
+#pragma unroll
+      for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+        for (int j = 0; j < kBcaQMax; ++j)
+          if (i < q && j < q) wv[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
+      for (int tt = ts; tt < ntok; tt += TS) {
+        BinPair xv[kBcaQMax], gv[kBcaQMax];
+#pragma unroll
+        for (int j = 0; j < kBcaQMax; ++j)
+          if (j < q) {
+            xv[j] = bins_get(Hx + P::row(tt * q + j), oa, ob, special);
+            gv[j] = bins_get(Hg + P::row(tt * q + j), oa, ob, special);
+          }
+#pragma unroll
+        for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+          for (int j = 0; j < kBcaQMax; ++j)
+            if (i < q && j < q) {
+              acc[a][i][j].b1 = special ? rfma(xv[j].b1, gv[i].b1, acc[a][i][j].b1)
+                                        : cfmac(xv[j].b1, gv[i].b1, acc[a][i][j].b1);
+              acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
+            }
+#pragma unroll
+        for (int j = 0; j < kBcaQMax; ++j) {
+          if (j < q) {
+            BinPair d = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+            for (int i = 0; i < kBcaQMax; ++i)
+              if (i < q) {
+                d.b1 = special ? rfma(wv[i][j].b1, gv[i].b1, d.b1) : cfmac(wv[i][j].b1, gv[i].b1, d.b1);
+                d.b2 = cfmac(wv[i][j].b2, gv[i].b2, d.b2);
+              }
+            bins_put(Hx + P::row(tt * q + j), oa, ob, special, d);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    p2_last_inv<P>(rx, nv);
+    p2_dc_inv<P>(rx, nv);
+    __syncthreads();
+    p2_pass1_inv<P>(rx, dx + tile * TT * tok_elems, nv);  // g rows of this tile are already consumed
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < IPT; ++a) {
+    const int u = (tid % NI) + a * NT;
+#pragma unroll
+    for (int i = 0; i < kBcaQMax; ++i)
+#pragma unroll
+      for (int j = 0; j < kBcaQMax; ++j) {
+        if (i < q && j < q) {
+          float* d = dw + (int64_t)(i * q + j) * N;
+          const BinPair v = acc[a][i][j];
+          if (u == 0) {
+            atomicAdd(d + 0, v.b1.x);
+            atomicAdd(d + N / 2, v.b1.y);
+            atomicAdd(d + N / 4, v.b2.x);
+            atomicAdd(d + 3 * N / 4, v.b2.y);
+          } else {
+            atomicAdd(d + u, v.b1.x);
+            atomicAdd(d + N - u, v.b1.y);
+            atomicAdd(d + N / 2 - u, v.b2.x);
+            atomicAdd(d + N / 2 + u, v.b2.y);
+          }
+        }
+      }
+  }
+}
+
+template <typename P>
+bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
+                     typename P::elem* dx, float* dw, int64_t T_, int q, int sms, cudaStream_t st) {
+  using L = BcaBwd3Smem<P>;
+  auto k = bca_bwd3_kernel<P>;
+  const int TT = P::VT / q;
+  const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
+  if (grid <= 0) return false;
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, q);
+  return true;
+}
+
+// ------------------------------------------------------------------ dispatch
 
 template <typename P>
 bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int q,
@@ -454,7 +615,7 @@ bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t 
   switch (p) {
     case 256: return launch_bca_bwd2<Plan2<T, 256, 16, 16>>(x, w, g, dx, dw, T_, q_in, sms, st);
     case 512: return launch_bca_bwd2<Plan2<T, 512, 32, 8>>(x, w, g, dx, dw, T_, q_in, sms, st);
-    case 1024: return launch_bca_bwd2<Plan2<T, 1024, 32, 8>>(x, w, g, dx, dw, T_, q_in, sms, st);
+    case 1024: return launch_bca_bwd3<Plan2<T, 1024, 32, 16>>(x, w, g, dx, dw, T_, q_in, sms, st);
     default: return false;
   }
 }
