@@ -396,10 +396,18 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
 
 template <typename P, typename K>
 int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (smem > 227 * 1024) return 0;  // configuration does not fit: caller falls back
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
   if (per_sm <= 0) return 0;
   return (int)(units < (int64_t)per_sm * sms ? units : (int64_t)per_sm * sms);
 }
@@ -603,7 +611,9 @@ bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out,
   switch (p) {
     case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>>(x, w, y, T_, q_in, sms, st);
     case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>>(x, w, y, T_, q_in, sms, st);
-    case 1024: return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, RDFFT_BCA_FWD_NSTG>>(x, w, y, T_, q_in, sms, st);
+    case 1024:
+      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>>(
+          x, w, y, T_, q_in, sms, st);
     default: return false;
   }
 }

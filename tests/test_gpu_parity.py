@@ -197,7 +197,9 @@ def test_packed_mul_spec_examples(cuda_device):
 
 
 # ------------------------------------------------------------------ BCA layer
-BCA_SHAPES = [(1, 1, 2), (1, 1, 4), (2, 3, 8), (4, 2, 16), (3, 3, 64), (3, 3, 256), (4, 4, 1024), (2, 1, 4096)]
+# fused fast paths: square q <= 4 with p in {256, 512, 1024}; the rest exercises the generic kernels
+BCA_SHAPES = [(1, 1, 2), (1, 1, 4), (2, 3, 8), (4, 2, 16), (3, 3, 64), (1, 1, 256), (3, 3, 256), (4, 4, 256),
+              (2, 2, 512), (1, 1, 1024), (2, 2, 1024), (3, 3, 1024), (4, 4, 1024), (2, 1, 4096)]
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -264,3 +266,44 @@ def test_errors_raise(cuda_device):
         R.rdfft_fwd(torch.zeros(4, 16, device="cuda", dtype=torch.float16))
     with pytest.raises(ValueError):
         R.rdfft_fwd(torch.zeros(4, 16))
+
+
+# ---------------------------------------------------------------- full bench sizes, sampled
+def test_full_size_transform_sampled():
+    """BASELINE configs[1] at the metric's n: 2^20 x 1024 bf16, the launch configuration bench.py times;
+    sampled rows against the oracle, forward then inverse (round trip on every row)."""
+    b, n = 1 << 20, 1024
+    x = synth.randn((b, n), seed=77, dtype="bf16", device="cuda")
+    idx = torch.tensor(sorted({0, 1, b // 2, b - 2, b - 1, *np.random.default_rng(7).integers(0, b, 40).tolist()}),
+                       device="cuda")
+    xin = f64(x[idx])
+    x0 = x.clone()
+    R.rdfft_fwd(x)
+    torch.cuda.synchronize()
+    assert rel_l2_rows(f64(x[idx]), o.rdfft_fwd(xin)) <= 2e-2
+    pin = f64(x[idx])
+    R.rdfft_inv(x)
+    torch.cuda.synchronize()
+    assert rel_l2_rows(f64(x[idx]), o.rdfft_inv(pin)) <= 2e-2
+    err = (x.float() - x0.float()).norm(dim=1) / x0.float().norm(dim=1)
+    assert float(err.max()) <= 2e-2
+
+
+def test_full_size_bca_sampled():
+    """BASELINE configs[3] (LLaMA2-7B adapter, T = 16384, d = 4096, p = 1024, bf16): sampled token rows
+    of y and dx against the oracle; dw by additivity over token halves (dw is a sum over tokens)."""
+    T, d, p = 8 * 2048, 4096, 1024
+    x, w, g = synth.bca_inputs(T, d, d, p, seed=11, dtype="bf16", device="cuda")
+    rows = torch.tensor(sorted({0, 5, T // 2, T - 1, *np.random.default_rng(3).integers(0, T, 6).tolist()}),
+                        device="cuda")
+    y = R.bca_fwd(x, w)
+    dx, dw = R.bca_bwd(x, w, g)
+    _, dw_a = R.bca_bwd(x[: T // 2].contiguous(), w, g[: T // 2].contiguous())
+    _, dw_b = R.bca_bwd(x[T // 2:].contiguous(), w, g[T // 2:].contiguous())
+    torch.cuda.synchronize()
+    xo, wo, go = f64(x[rows]), f64(w), f64(g[rows])
+    assert rel_l2_rows(f64(y[rows]), o.bca_fwd(xo, wo)) <= 2e-2
+    dxo, _ = o.bca_bwd(xo, wo, go)
+    assert rel_l2_rows(f64(dx[rows]), dxo) <= 2e-2
+    s = (dw_a + dw_b).double()
+    assert float((dw.double() - s).norm() / s.norm()) <= 1e-5
