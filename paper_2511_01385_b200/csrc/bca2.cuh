@@ -145,14 +145,11 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
   }
   const uint32_t k65536 = kTwo16;
   const P2Roles<P> rh(H, TWf, TWi, tid);
-  auto tile_bytes = [&](int64_t t) {
-    const int64_t nt = T_ - t * TT < TT ? T_ - t * TT : TT;
-    return (uint32_t)(nt * tok_elems * (int)sizeof(T));
-  };
+  auto tile_rows = [&](int64_t t) { return (int)((T_ - t * TT < TT ? T_ - t * TT : TT) * q); };
   __syncthreads();
   // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors, into the resident region
   if constexpr (L::STAGES > 0) {
-    if (tid == 0) stage_issue(w, (uint32_t)(q * q * N * (int)sizeof(T)), base, bar);
+    if (tid == 0) stage_issue_rows<P>(w, q * q, base, bar);
     mbar_wait(bar, 0);
   }
   {
@@ -170,7 +167,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
   if (tid == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
       const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
-      if (t < ntiles) stage_issue(x + t * TT * tok_elems, tile_bytes(t), base + s * P::STAGE, bar + s);
+      if (t < ntiles) stage_issue_rows<P>(x + t * TT * tok_elems, tile_rows(t), base + s * P::STAGE, bar + s);
     }
   }
   int it = 0;
@@ -189,7 +186,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
       __syncthreads();  // H complete, staging sb consumed
       const int64_t nxt = tile + (int64_t)L::STAGES * gridDim.x;
       if (tid == 0 && nxt < ntiles)
-        stage_issue(x + nxt * TT * tok_elems, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+        stage_issue_rows<P>(x + nxt * TT * tok_elems, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
     }
     p2_last_fwd<P>(rh, nv);
     p2_dc_fwd<P>(rh, nv);
@@ -254,10 +251,7 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
   }
   const uint32_t k65536 = kTwo16;
   const P2Roles<P> rh(Hm, TWf, TWi, lt);
-  auto tile_bytes = [&](int64_t t) {
-    const int64_t nt = T_ - t * TT < TT ? T_ - t * TT : TT;
-    return (uint32_t)(nt * tok_elems * (int)sizeof(T));
-  };
+  auto tile_rows = [&](int64_t t) { return (int)((T_ - t * TT < TT ? T_ - t * TT : TT) * q); };
   __syncthreads();
   // ---- prologue: W_ij = rdFFT(w_ij) into the resident region.  q*q <= VT: group 0 does all
   // rows; q*q = 16 > VT = 8: rows [0, 8) by group 0 and [8, 16) by group 1 (8 = skew period,
@@ -265,7 +259,7 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
   const int nw = q * q;
   const int half = nw <= P::VT ? nw : 8;
   const int w0 = grp ? half : 0, wn = grp ? nw - half : half;
-  if (lt == 0 && wn > 0) stage_issue(w + (int64_t)w0 * N, (uint32_t)(wn * N * (int)sizeof(T)), stg, gbar);
+  if (lt == 0 && wn > 0) stage_issue_rows<P>(w + (int64_t)w0 * N, wn, stg, gbar);
   if (wn > 0) mbar_wait(gbar, 0);
   {
     const P2Roles<P> rw(Wr + w0 * P::ROWA, TWf, TWi, lt);
@@ -279,7 +273,7 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
   if (lt == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
       const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
-      if (t < ntiles) stage_issue(src + t * TT * tok_elems, tile_bytes(t), stg + s * P::STAGE, gbar + s);
+      if (t < ntiles) stage_issue_rows<P>(src + t * TT * tok_elems, tile_rows(t), stg + s * P::STAGE, gbar + s);
     }
   }
   // dW accumulators: item u = tid (one item per thread when 2 NT == N/4), all q*q pairs, 2 bins
@@ -305,7 +299,7 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
     __syncthreads();
     const int64_t nxt = tile + (int64_t)L::STAGES * gridDim.x;
     if (lt == 0 && nxt < ntiles)
-      stage_issue(src + nxt * TT * tok_elems, tile_bytes(nxt), stg + sb * P::STAGE, gbar + sb);
+      stage_issue_rows<P>(src + nxt * TT * tok_elems, tile_rows(nxt), stg + sb * P::STAGE, gbar + sb);
     p2_last_fwd<P>(rh, nv);
     p2_dc_fwd<P>(rh, nv);
     __syncthreads();

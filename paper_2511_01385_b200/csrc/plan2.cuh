@@ -95,9 +95,12 @@ struct Plan2 {
   static constexpr int NWIN = S / 2;        // windows per row (first half of the slots)
   static constexpr int ROWA = ((NWIN * WSTR + 14 + 15) / 16) * 16;  // room for the row skew (<= 14)
   static constexpr int HF = VT * ROWA + 16;  // float2 in one H region
-  static constexpr int TWF = M * LPV;
+  static constexpr int TWS = M + 2;         // twiddle row (one per k), padded: 16-byte pair loads, no conflicts
+  static constexpr int TWF = LPV * TWS;
   static constexpr int CHV = N / 4;         // 16-byte H chunks per vector
-  static constexpr int STAGE = VT * N * (int)sizeof(T);
+  // staged rows are skewed by 64 bytes: the two vectors of a warp read complementary bank halves
+  static constexpr int SROW = N + 64 / (int)sizeof(T);
+  static constexpr int STAGE = VT * SROW * (int)sizeof(T);
   static_assert(M <= R && M >= 4 && (R == 32 || R == 16), "2-pass plan shape");
   static_assert(NT % 32 == 0 && VT * P1 <= NT, "thread mapping");
   static_assert(VT <= 32, "one DC-set lane per vector in the last warp");
@@ -117,7 +120,7 @@ struct Plan2 {
 template <typename P>
 struct P2Roles {
   float2* h1;        // pass 1: window w1 of vector v1
-  int v1, s1;        //   element offset of subsequence 2 c1 in a tile
+  int v1, s1, s1s;   //   element offset of subsequence 2 c1 in a global / staged tile
   bool act1;
   int v2, k;         // last pass: vector v2, set k
   float2* ha;        //   slots j R + k
@@ -138,13 +141,14 @@ struct P2Roles {
     act1 = lt < P::VT * P::P1;
     h1 = H + P::row(v1) + w1 * P::WSTR;
     s1 = v1 * P::N + 2 * c1;
+    s1s = v1 * P::SROW + 2 * c1;
     v2 = lt / P::LPV;
     k = 1 + lt % P::LPV;
     ha = H + P::row(v2) + k;
     hm = H + P::row(v2) + (R - k);
     hmz = (k == R / 2) ? (H + P::row(v2) + R) : hm;
-    twf = TWf + (k - 1);
-    twi = TWi + (k - 1);
+    twf = TWf + (k - 1) * P::TWS;
+    twi = TWi + (k - 1) * P::TWS;
     dv = lt - (P::NT - 32);
     hd = H + P::row(dv < 0 ? 0 : dv);
     vq = (P::CHV < P::NT) ? lt / P::CHV : 0;
@@ -153,11 +157,12 @@ struct P2Roles {
   }
 };
 
-// Twiddle tables and pads (whole CTA): TWf[j LPV + k-1] = W_N^{k rev(j)}, TWi = conj(.)/N.
+// Twiddle tables and pads (whole CTA): TWf[(k-1) TWS + j] = W_N^{k rev(j)}, TWi = conj(.)/N.
 template <typename P>
 __device__ __forceinline__ void p2_tables(float2* TWf, float2* TWi, int tid, int nthreads) {
   for (int e = tid; e < P::TWF; e += nthreads) {
-    const int j = e / P::LPV, k = 1 + e % P::LPV;
+    const int k = 1 + e / P::TWS, j = e % P::TWS;
+    if (j >= P::M) continue;
     float s, c;
     sincospif(2.0f * (float)(k * rev_bits<P::LM>(j)) / (float)P::N, &s, &c);
     if (TWf) TWf[e] = make_float2(c, -s);
@@ -182,7 +187,7 @@ __device__ __forceinline__ void p2_pass1_fwd(const P2Roles<P>& r, const typename
   constexpr int R = P::R, S = P::S;
   if (r.act1 && r.v1 < nv) {
     float2 b[R];
-    const T* src = st + r.s1;
+    const T* src = st + (kGlobal ? r.s1 : r.s1s);
     ct::static_for<0, R>([&](auto I) {
       constexpr int i = decltype(I)::value;
       if constexpr (kGlobal)
@@ -212,12 +217,17 @@ __device__ __forceinline__ void p2_last_fwd(const P2Roles<P>& r, int nv) {
       zi[jj] = bb.x;
       zi[jj + M / 2] = bb.y;
     });
-    ct::static_for<1, M>([&](auto J) {
-      constexpr int j = decltype(J)::value;
-      const float2 t = r.twf[j * P::LPV];
-      const float q = zr[j];
-      zr[j] = fmaf(q, t.x, -zi[j] * t.y);
-      zi[j] = fmaf(q, t.y, zi[j] * t.x);
+    ct::static_for<0, M / 2>([&](auto J2) {
+      constexpr int j0 = 2 * decltype(J2)::value;
+      const float4 t2 = *reinterpret_cast<const float4*>(r.twf + j0);
+      if constexpr (j0 > 0) {
+        const float q = zr[j0];
+        zr[j0] = fmaf(q, t2.x, -zi[j0] * t2.y);
+        zi[j0] = fmaf(q, t2.y, zi[j0] * t2.x);
+      }
+      const float q1 = zr[j0 + 1];
+      zr[j0 + 1] = fmaf(q1, t2.z, -zi[j0 + 1] * t2.w);
+      zi[j0 + 1] = fmaf(q1, t2.w, zi[j0 + 1] * t2.z);
     });
     cfft_dit<M>(zr, zi);
     ct::static_for<0, M / 2>([&](auto Q) {
@@ -288,7 +298,7 @@ __device__ __forceinline__ void p2_load(const P2Roles<P>& r, const typename P::e
   using T = typename P::elem;
   p2_chunks<P>(r, [&](int vv, int t, const float2* h) {
     if (vv < nv) {
-      const T* src = st + vv * P::N + 2 * t;
+      const T* src = st + vv * P::SROW + 2 * t;
       const float2 lo = sio<T>::ld2(src, k65536);
       const float2 hi = sio<T>::ld2(src + P::N / 2, k65536);
       *reinterpret_cast<float4*>(const_cast<float2*>(h)) = make_float4(lo.x, hi.x, lo.y, hi.y);
@@ -313,13 +323,16 @@ __device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv) {
       zi[rev_bits<LM>(q)] = bb.y;
     });
     cfft_dit<M, true>(zr, zi);
-    ct::static_for<0, M>([&](auto J) {
-      constexpr int j = decltype(J)::value;
-      constexpr int rj = rev_bits<LM>(j);
-      const float2 t = r.twi[j * P::LPV];
-      const float q = zr[rj];
-      zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
-      zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
+    ct::static_for<0, M / 2>([&](auto J2) {
+      constexpr int j0 = 2 * decltype(J2)::value;
+      constexpr int r0 = rev_bits<LM>(j0), r1 = rev_bits<LM>(j0 + 1);
+      const float4 t2 = *reinterpret_cast<const float4*>(r.twi + j0);
+      const float q0 = zr[r0];
+      zr[r0] = fmaf(q0, t2.x, -zi[r0] * t2.y);
+      zi[r0] = fmaf(q0, t2.y, zi[r0] * t2.x);
+      const float q1 = zr[r1];
+      zr[r1] = fmaf(q1, t2.z, -zi[r1] * t2.w);
+      zi[r1] = fmaf(q1, t2.w, zi[r1] * t2.z);
     });
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
@@ -378,6 +391,15 @@ __device__ __forceinline__ void stage_issue(const T* src, uint32_t bytes, void* 
   mbar_arrive_expect_tx(bar, bytes);
   bulk_g2s(dst, src, bytes, bar);
 }
+// nrows rows of n elements -> staged rows of SROW elements (one bulk copy per row)
+template <typename P>
+__device__ __forceinline__ void stage_issue_rows(const typename P::elem* src, int nrows, void* dst, uint64_t* bar) {
+  using T = typename P::elem;
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(bar, (uint32_t)(nrows * P::N * (int)sizeof(T)));
+  for (int v = 0; v < nrows; ++v)
+    bulk_g2s(reinterpret_cast<T*>(dst) + v * P::SROW, src + (int64_t)v * P::N, (uint32_t)(P::N * sizeof(T)), bar);
+}
 
 // ---------------------------------------------------------------- rdfft kernels
 template <typename P>
@@ -408,17 +430,14 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   const P2Roles<P> r(H, TW, TW, tid);
   const uint32_t k65536 = kTwo16;
   const int64_t ntiles = (batch + VT - 1) / VT;
-  auto tile_bytes = [&](int64_t t) {
-    const int64_t nv = batch - t * VT < VT ? batch - t * VT : VT;
-    return (uint32_t)(nv * N * (int)sizeof(T));
-  };
+  auto tile_rows = [&](int64_t t) { return (int)(batch - t * VT < VT ? batch - t * VT : VT); };
   __syncthreads();
   constexpr int NS = P::NSTG;
   static_assert(!(kInv && NS == 0), "the inverse transform stages its input");
   if (tid == 0) {
     for (int q = 0; q < NS; ++q) {
       const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
-      if (t < ntiles) stage_issue(x + t * VT * (int64_t)N, tile_bytes(t), base + q * P::STAGE, bar + q);
+      if (t < ntiles) stage_issue_rows<P>(x + t * VT * (int64_t)N, tile_rows(t), base + q * P::STAGE, bar + q);
     }
   }
   int it = 0;
@@ -440,7 +459,7 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
       if (!kInv) {
         p2_pass1_fwd<P>(r, st, nv, k65536);
         __syncthreads();  // H complete; staging buffer sb consumed
-        if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+        if (tid == 0 && nxt < ntiles) stage_issue_rows<P>(x + nxt * VT * (int64_t)N, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
         p2_last_fwd<P>(r, nv);
         p2_dc_fwd<P>(r, nv);
         __syncthreads();
@@ -448,7 +467,7 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
       } else {
         p2_load<P>(r, st, nv, k65536);
         __syncthreads();
-        if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+        if (tid == 0 && nxt < ntiles) stage_issue_rows<P>(x + nxt * VT * (int64_t)N, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
         p2_last_inv<P>(r, nv);
         p2_dc_inv<P>(r, nv);
         __syncthreads();
