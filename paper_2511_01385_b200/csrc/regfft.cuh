@@ -75,23 +75,28 @@ __device__ __forceinline__ void rfft_fwd_reg(V (&b)[R]) {
 }
 
 // Packed spectrum -> R x (bit-reversed real sequence).  Unscaled (see header).
+// The doubling of the k = m/2 slots is folded into the next stage: those slots are exactly the
+// k = 0 partners (b[be + m]) of the following stage, which then combines a +- 2c with one FFMA.
 template <int R, typename V>
 __device__ __forceinline__ void rfft_inv_reg(V (&b)[R]) {
   ct::static_for<0, 31>([&](auto LI) {
     constexpr int lm = 30 - decltype(LI)::value;  // descending stage order
     constexpr int m = 1 << lm;
     if constexpr (m < R) {
+      constexpr bool first = (2 * m == R);  // inputs all at the same scale
       ct::static_for<0, R / (2 * m)>([&](auto BB) {
         constexpr int be = decltype(BB)::value * 2 * m;
         {
           const V a = b[be], c = b[be + m];
-          b[be] = a + c;
-          b[be + m] = a - c;
+          if constexpr (first) {
+            b[be] = a + c;
+            b[be + m] = a - c;
+          } else {  // c is an undoubled k = m/2 slot of the previous stage
+            b[be] = fma2s(c, 2.0f, a);
+            b[be + m] = fma2s(c, -2.0f, a);
+          }
         }
-        if constexpr (m >= 2) {
-          b[be + m / 2] = b[be + m / 2] + b[be + m / 2];
-          b[be + 3 * m / 2] = -(b[be + 3 * m / 2] + b[be + 3 * m / 2]);
-        }
+        if constexpr (m >= 2) b[be + 3 * m / 2] = -b[be + 3 * m / 2];  // k = m/2: sign only
         ct::static_for<1, m / 2>([&](auto KK) {
           constexpr int k = decltype(KK)::value;
           // B = (Yk - Y_{m+k}) conj(W): conj(W) = (wr, -wi)
