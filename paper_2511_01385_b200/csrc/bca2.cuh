@@ -80,8 +80,9 @@ __device__ __forceinline__ void bca_item_offsets(int u, int& oa, int& ob) {
 }
 
 // In-place forward product over one tile: Y_i = sum_j W_ij (.) X_j for tokens of this tile.
-template <typename P>
-__device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int q, int ntok, int tid) {
+template <typename P, int Q>
+__device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int ntok, int tid) {
+  constexpr int q = Q;
   constexpr int NI = P::N / 4;
   constexpr int TS = P::NT >= NI ? P::NT / NI : 1;  // thread groups sharing an item (token split)
   for (int u = tid % NI; u < NI; u += (P::NT >= NI ? NI : P::NT)) {
@@ -89,23 +90,23 @@ __device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int
     int oa, ob;
     bca_item_offsets<P>(u, oa, ob);
     const bool special = (u == 0);
-    BinPair w[kBcaQMax][kBcaQMax];
+    BinPair w[Q][Q];
 #pragma unroll
-    for (int i = 0; i < kBcaQMax; ++i)
+    for (int i = 0; i < Q; ++i)
 #pragma unroll
-      for (int j = 0; j < kBcaQMax; ++j)
+      for (int j = 0; j < Q; ++j)
         if (i < q && j < q) w[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
     for (int tt = ts; tt < ntok; tt += TS) {
-      BinPair x[kBcaQMax];
+      BinPair x[Q];
 #pragma unroll
-      for (int j = 0; j < kBcaQMax; ++j)
+      for (int j = 0; j < Q; ++j)
         if (j < q) x[j] = bins_get(H + P::row(tt * q + j), oa, ob, special);
 #pragma unroll
-      for (int i = 0; i < kBcaQMax; ++i) {
+      for (int i = 0; i < Q; ++i) {
         if (i < q) {
           BinPair y = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-          for (int j = 0; j < kBcaQMax; ++j) {
+          for (int j = 0; j < Q; ++j) {
             if (j < q) {
               y.b1 = special ? rfma(w[i][j].b1, x[j].b1, y.b1) : cfma(w[i][j].b1, x[j].b1, y.b1);
               y.b2 = cfma(w[i][j].b2, x[j].b2, y.b2);
@@ -118,10 +119,11 @@ __device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int
   }
 }
 
-template <typename P>
+template <typename P, int Q>
 __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::elem* __restrict__ x,
                                                          const typename P::elem* __restrict__ w,
-                                                         typename P::elem* __restrict__ y, int64_t T_, int q) {
+                                                         typename P::elem* __restrict__ y, int64_t T_) {
+  constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaFwdSmem<P>;
   constexpr int N = P::N;
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
     p2_last_fwd<P>(rh, nv);
     p2_dc_fwd<P>(rh, nv);
     __syncthreads();
-    bca_product_fwd<P>(H, Wr, q, ntok, tid);
+    bca_product_fwd<P, Q>(H, Wr, ntok, tid);
     __syncthreads();
     p2_last_inv<P>(rh, nv);
     p2_dc_inv<P>(rh, nv);
@@ -216,11 +218,12 @@ struct BcaBwdSmem {  // [sx x STAGES][sg x STAGES][Hx][Hg][W][TWf][TWi][bars x 2
   static constexpr size_t BYTES = BAR_OFF + 32;
 };
 
-template <typename P>
+template <typename P, int Q>
 __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::elem* __restrict__ x,
                                                              const typename P::elem* __restrict__ w,
                                                              const typename P::elem* g, typename P::elem* dx,
-                                                             float* __restrict__ dw, int64_t T_, int q) {
+                                                             float* __restrict__ dw, int64_t T_) {
+  constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaBwdSmem<P>;
   constexpr int N = P::N, NT2 = 2 * P::NT, NI = N / 4;
@@ -280,13 +283,13 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
   static_assert(NT2 % NI == 0 || NI % NT2 == 0, "item mapping");
   constexpr int IPT = NI > NT2 ? NI / NT2 : 1;  // items per thread
   constexpr int TS = NT2 >= NI ? NT2 / NI : 1;   // token split
-  BinPair acc[IPT][kBcaQMax][kBcaQMax];
+  BinPair acc[IPT][Q][Q];
 #pragma unroll
   for (int a = 0; a < IPT; ++a)
 #pragma unroll
-    for (int i = 0; i < kBcaQMax; ++i)
+    for (int i = 0; i < Q; ++i)
 #pragma unroll
-      for (int j = 0; j < kBcaQMax; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      for (int j = 0; j < Q; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
@@ -311,35 +314,35 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
       int oa, ob;
       bca_item_offsets<P>(u, oa, ob);
       const bool special = (u == 0);
-      BinPair wv[kBcaQMax][kBcaQMax];
+      BinPair wv[Q][Q];
 #pragma unroll
-      for (int i = 0; i < kBcaQMax; ++i)
+      for (int i = 0; i < Q; ++i)
 #pragma unroll
-        for (int j = 0; j < kBcaQMax; ++j)
+        for (int j = 0; j < Q; ++j)
           if (i < q && j < q) wv[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
       for (int tt = ts; tt < ntok; tt += TS) {
-        BinPair xv[kBcaQMax], gv[kBcaQMax];
+        BinPair xv[Q], gv[Q];
 #pragma unroll
-        for (int j = 0; j < kBcaQMax; ++j)
+        for (int j = 0; j < Q; ++j)
           if (j < q) {
             xv[j] = bins_get(Hx + P::row(tt * q + j), oa, ob, special);
             gv[j] = bins_get(Hg + P::row(tt * q + j), oa, ob, special);
           }
 #pragma unroll
-        for (int i = 0; i < kBcaQMax; ++i)
+        for (int i = 0; i < Q; ++i)
 #pragma unroll
-          for (int j = 0; j < kBcaQMax; ++j)
+          for (int j = 0; j < Q; ++j)
             if (i < q && j < q) {
               acc[a][i][j].b1 = special ? rfma(xv[j].b1, gv[i].b1, acc[a][i][j].b1)
                                         : cfmac(xv[j].b1, gv[i].b1, acc[a][i][j].b1);
               acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
             }
 #pragma unroll
-        for (int j = 0; j < kBcaQMax; ++j) {
+        for (int j = 0; j < Q; ++j) {
           if (j < q) {
             BinPair d = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-            for (int i = 0; i < kBcaQMax; ++i)
+            for (int i = 0; i < Q; ++i)
               if (i < q) {
                 d.b1 = special ? rfma(wv[i][j].b1, gv[i].b1, d.b1) : cfmac(wv[i][j].b1, gv[i].b1, d.b1);
                 d.b2 = cfmac(wv[i][j].b2, gv[i].b2, d.b2);
@@ -366,9 +369,9 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
     const int ts = NT2 >= NI ? tid / NI : 0;
     (void)ts;
 #pragma unroll
-    for (int i = 0; i < kBcaQMax; ++i)
+    for (int i = 0; i < Q; ++i)
 #pragma unroll
-      for (int j = 0; j < kBcaQMax; ++j) {
+      for (int j = 0; j < Q; ++j) {
         if (i < q && j < q) {
           float* d = dw + (int64_t)(i * q + j) * N;
           const BinPair v = acc[a][i][j];
@@ -403,6 +406,9 @@ int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
     return 0;
   }
   if (per_sm <= 0) return 0;
+  if (verbose())
+    std::fprintf(stderr, "[rdfft] bca kernel p=%d VT=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N, P::VT, smem,
+                 threads, per_sm);
   return (int)(units < (int64_t)per_sm * sms ? units : (int64_t)per_sm * sms);
 }
 
@@ -421,11 +427,12 @@ struct BcaBwd3Smem {
   static constexpr size_t BYTES = TWI_OFF + (size_t)P::TWF * 8;
 };
 
-template <typename P>
+template <typename P, int Q>
 __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::elem* __restrict__ x,
                                                             const typename P::elem* __restrict__ w,
                                                             const typename P::elem* g, typename P::elem* dx,
-                                                            float* __restrict__ dw, int64_t T_, int q) {
+                                                            float* __restrict__ dw, int64_t T_) {
+  constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaBwd3Smem<P>;
   constexpr int N = P::N, NT = P::NT, NI = N / 4;
@@ -458,13 +465,13 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
   static_assert(NT % NI == 0 || NI % NT == 0, "item mapping");
   constexpr int IPT = NI > NT ? NI / NT : 1;  // items per thread
   constexpr int TS = NT >= NI ? NT / NI : 1;   // token split
-  BinPair acc[IPT][kBcaQMax][kBcaQMax];
+  BinPair acc[IPT][Q][Q];
 #pragma unroll
   for (int a = 0; a < IPT; ++a)
 #pragma unroll
-    for (int i = 0; i < kBcaQMax; ++i)
+    for (int i = 0; i < Q; ++i)
 #pragma unroll
-      for (int j = 0; j < kBcaQMax; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      for (int j = 0; j < Q; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
     const int nv = ntok * q;
@@ -483,35 +490,35 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
       int oa, ob;
       bca_item_offsets<P>(u, oa, ob);
       const bool special = (u == 0);
-      BinPair wv[kBcaQMax][kBcaQMax];
+      BinPair wv[Q][Q];
 #pragma unroll
-      for (int i = 0; i < kBcaQMax; ++i)
+      for (int i = 0; i < Q; ++i)
 #pragma unroll
-        for (int j = 0; j < kBcaQMax; ++j)
+        for (int j = 0; j < Q; ++j)
           if (i < q && j < q) wv[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
       for (int tt = ts; tt < ntok; tt += TS) {
-        BinPair xv[kBcaQMax], gv[kBcaQMax];
+        BinPair xv[Q], gv[Q];
 #pragma unroll
-        for (int j = 0; j < kBcaQMax; ++j)
+        for (int j = 0; j < Q; ++j)
           if (j < q) {
             xv[j] = bins_get(Hx + P::row(tt * q + j), oa, ob, special);
             gv[j] = bins_get(Hg + P::row(tt * q + j), oa, ob, special);
           }
 #pragma unroll
-        for (int i = 0; i < kBcaQMax; ++i)
+        for (int i = 0; i < Q; ++i)
 #pragma unroll
-          for (int j = 0; j < kBcaQMax; ++j)
+          for (int j = 0; j < Q; ++j)
             if (i < q && j < q) {
               acc[a][i][j].b1 = special ? rfma(xv[j].b1, gv[i].b1, acc[a][i][j].b1)
                                         : cfmac(xv[j].b1, gv[i].b1, acc[a][i][j].b1);
               acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
             }
 #pragma unroll
-        for (int j = 0; j < kBcaQMax; ++j) {
+        for (int j = 0; j < Q; ++j) {
           if (j < q) {
             BinPair d = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-            for (int i = 0; i < kBcaQMax; ++i)
+            for (int i = 0; i < Q; ++i)
               if (i < q) {
                 d.b1 = special ? rfma(wv[i][j].b1, gv[i].b1, d.b1) : cfmac(wv[i][j].b1, gv[i].b1, d.b1);
                 d.b2 = cfmac(wv[i][j].b2, gv[i].b2, d.b2);
@@ -532,9 +539,9 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
   for (int a = 0; a < IPT; ++a) {
     const int u = (tid % NI) + a * NT;
 #pragma unroll
-    for (int i = 0; i < kBcaQMax; ++i)
+    for (int i = 0; i < Q; ++i)
 #pragma unroll
-      for (int j = 0; j < kBcaQMax; ++j) {
+      for (int j = 0; j < Q; ++j) {
         if (i < q && j < q) {
           float* d = dw + (int64_t)(i * q + j) * N;
           const BinPair v = acc[a][i][j];
@@ -554,41 +561,41 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
   }
 }
 
-template <typename P>
+template <typename P, int Q>
 bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
-                     typename P::elem* dx, float* dw, int64_t T_, int q, int sms, cudaStream_t st) {
+                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
   using L = BcaBwd3Smem<P>;
-  auto k = bca_bwd3_kernel<P>;
-  const int TT = P::VT / q;
+  auto k = bca_bwd3_kernel<P, Q>;
+  constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, q);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_);
   return true;
 }
 
 // ------------------------------------------------------------------ dispatch
 
-template <typename P>
-bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int q,
-                     int sms, cudaStream_t st) {
+template <typename P, int Q>
+bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
+                     cudaStream_t st) {
   using L = BcaFwdSmem<P>;
-  auto k = bca_fwd2_kernel<P>;
-  const int TT = P::VT / q;
+  auto k = bca_fwd2_kernel<P, Q>;
+  constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_, q);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_);
   return true;
 }
 
-template <typename P>
+template <typename P, int Q>
 bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
-                     typename P::elem* dx, float* dw, int64_t T_, int q, int sms, cudaStream_t st) {
+                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
   using L = BcaBwdSmem<P>;
-  auto k = bca_bwd2_kernel<P>;
-  const int TT = P::VT / q;
+  auto k = bca_bwd2_kernel<P, Q>;
+  constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, 2 * P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, q);
+  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_);
   return true;
 }
 
@@ -599,15 +606,36 @@ bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const
 #define RDFFT_BCA_FWD_NSTG 2  // ... with pass 1 reading x straight from HBM (H + W fill shared memory)
 #endif
 // Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
+template <typename T, int Q>
+bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st) {
+  switch (p) {
+    case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
+    case 1024:
+      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
+          x, w, y, T_, sms, st);
+    default: return false;
+  }
+}
+template <typename T, int Q>
+bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
+                    cudaStream_t st) {
+  switch (p) {
+    case 256: return launch_bca_bwd2<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+    case 512: return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st);
+    case 1024: return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+    default: return false;
+  }
+}
+
 template <typename T>
 bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
-  if (q_in != q_out || q_in > kBcaQMax) return false;
-  switch (p) {
-    case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>>(x, w, y, T_, q_in, sms, st);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>>(x, w, y, T_, q_in, sms, st);
-    case 1024:
-      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>>(
-          x, w, y, T_, q_in, sms, st);
+  if (q_in != q_out) return false;
+  switch (q_in) {
+    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st);
+    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st);
+    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st);
+    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st);
     default: return false;
   }
 }
@@ -615,11 +643,12 @@ bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out,
 template <typename T>
 bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
                   int sms, cudaStream_t st) {
-  if (q_in != q_out || q_in > kBcaQMax) return false;
-  switch (p) {
-    case 256: return launch_bca_bwd2<Plan2<T, 256, 16, 16>>(x, w, g, dx, dw, T_, q_in, sms, st);
-    case 512: return launch_bca_bwd2<Plan2<T, 512, 32, 8>>(x, w, g, dx, dw, T_, q_in, sms, st);
-    case 1024: return launch_bca_bwd3<Plan2<T, 1024, 32, 16>>(x, w, g, dx, dw, T_, q_in, sms, st);
+  if (q_in != q_out) return false;
+  switch (q_in) {
+    case 1: return bca_bwd_fast_q<T, 1>(x, w, g, dx, dw, T_, p, sms, st);
+    case 2: return bca_bwd_fast_q<T, 2>(x, w, g, dx, dw, T_, p, sms, st);
+    case 3: return bca_bwd_fast_q<T, 3>(x, w, g, dx, dw, T_, p, sms, st);
+    case 4: return bca_bwd_fast_q<T, 4>(x, w, g, dx, dw, T_, p, sms, st);
     default: return false;
   }
 }

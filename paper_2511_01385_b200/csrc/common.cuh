@@ -9,7 +9,19 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace rdfft {
+
+// RDFFT_VERBOSE=1: report each kernel configuration (shared memory, CTAs per SM) once.
+inline bool verbose() {
+  static const bool v = [] {
+    const char* e = std::getenv("RDFFT_VERBOSE");
+    return e && *e && *e != '0';
+  }();
+  return v;
+}
 
 constexpr int kMaxN = 4096;
 constexpr int kMaxLogN = 12;

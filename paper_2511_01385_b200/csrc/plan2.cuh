@@ -489,6 +489,9 @@ bool launch_plan2_dir(typename P::elem* x, int64_t batch, int sms, cudaStream_t 
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NT, L::BYTES);
     if (per_sm < 1) per_sm = 1;
+    if (verbose())
+      std::fprintf(stderr, "[rdfft] plan2 n=%d R=%d VT=%d NSTG=%d inv=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N,
+                   P::R, P::VT, P::NSTG, (int)kInv, (size_t)L::BYTES, P::NT, per_sm);
   }
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);

@@ -395,6 +395,9 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
     per_sm = a < b ? a : b;
     if (per_sm < 1) per_sm = 1;
     configured = true;
+    if (verbose())
+      std::fprintf(stderr, "[rdfft] plan3 n=%d VT=%d NSTG=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N, P::VT,
+                   P::NSTG, (size_t)L::BYTES, P::NT, per_sm);
   }
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
