@@ -11,6 +11,7 @@
 #pragma once
 
 #include "plan2.cuh"
+#include "small.cuh"
 
 namespace rdfft {
 
@@ -416,7 +417,14 @@ template <typename T>
 bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st) {
   (void)logn;
   switch (n) {
-    case 64: return launch_plan2<Plan2<T, 64, 16, 32>, Plan2<T, 64, 16, 32>>(x, batch, inverse, sms, st);
+    case 2: return launch_small<T, 2>(x, batch, inverse, sms, st);
+    case 4: return launch_small<T, 4>(x, batch, inverse, sms, st);
+    case 8: return launch_small<T, 8>(x, batch, inverse, sms, st);
+    case 16: return launch_small<T, 16>(x, batch, inverse, sms, st);
+    case 32: return launch_small<T, 32>(x, batch, inverse, sms, st);
+    case 64:  // bf16 rows are 128 B (in-register path wins); fp32 rows (256 B) thrash L1 there
+      if (sizeof(T) == 2) return launch_small<T, 64>(x, batch, inverse, sms, st);
+      return launch_plan2<Plan2<T, 64, 16, 32>, Plan2<T, 64, 16, 32>>(x, batch, inverse, sms, st);
     case 128: return launch_plan2<Plan2<T, 128, 16, 16>, Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
     case 256: return launch_plan2<Plan2<T, 256, 16, 16>, Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
     case 512: return launch_plan2<Plan2<T, 512, 32, 8, RDFFT_FWD_NSTG>, Plan2<T, 512, 32, 8, 1>>(x, batch, inverse, sms, st);
