@@ -307,3 +307,21 @@ def test_full_size_bca_sampled():
     assert rel_l2_rows(f64(dx[rows]), dxo) <= 2e-2
     s = (dw_a + dw_b).double()
     assert float((dw.double() - s).norm() / s.norm()) <= 1e-5
+
+
+def test_host_pipeline_matches_device_calls():
+    from paper_2511_01385_b200 import pipeline as PL
+
+    b, n = 5000, 1024
+    x = synth.randn((b, n), seed=21, dtype="bf16")
+    xh = x.clone().pin_memory()
+    xd = torch.empty((b, n), dtype=torch.bfloat16, device="cuda")
+    filt = synth.randn((1, n), seed=22, dtype="bf16", device="cuda")
+    PL.fwd_inv_host(xh, xd, filt=filt, chunk_rows=1024)
+    torch.cuda.synchronize()
+    ref = x.cuda()
+    R.rdfft_fwd(ref)
+    R.rdfft_packed_mul(ref, filt)
+    R.rdfft_inv(ref)
+    torch.cuda.synchronize()
+    assert torch.equal(xh, ref.cpu())
