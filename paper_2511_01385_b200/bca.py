@@ -1,0 +1,56 @@
+"""Autograd wrapper of the fused BCA kernels.
+
+`BlockCirculantAdapter` is a block-circulant linear layer y = C x with C made of
+q_out x q_in circulant p x p blocks defined by their first columns w[i][j]
+(P:L165-184).  Forward and backward are the C-ABI calls `bca_fwd` / `bca_bwd`:
+no spectra are stored between them (the backward recomputes rdFFT(x) on chip),
+and the input gradient overwrites grad_output in place when the layer is square
+("by overwriting the grad_output in-place").  The weight gradient is
+accumulated in fp32 and cast to the parameter dtype for autograd.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import rdfft as R
+
+
+class BCAFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        x = x.contiguous()
+        ctx.save_for_backward(x, w)
+        return R.bca_fwd(x, w)
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        x, w = ctx.saved_tensors
+        g = g.contiguous()
+        q_out, q_in, _ = w.shape
+        # grad_output is overwritten by dx when d_in == d_out (zero extra activation memory)
+        dx = g if q_out == q_in else None
+        dx, dw = R.bca_bwd(x, w, g, dx)
+        return dx, (dw if w.dtype == torch.float32 else dw.to(w.dtype))
+
+
+def bca(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    return BCAFunction.apply(x, w)
+
+
+class BlockCirculantAdapter(torch.nn.Module):
+    """y = BCA(x) with weight [out/p, in/p, p] (first columns of the circulant blocks)."""
+
+    def __init__(self, d_in: int, d_out: int, p: int, dtype=torch.float32, device=None, init_std: float | None = None):
+        super().__init__()
+        if d_in % p or d_out % p:
+            raise ValueError("d_in and d_out must be multiples of the block size p")
+        std = init_std if init_std is not None else d_in ** -0.5
+        self.p = p
+        self.weight = torch.nn.Parameter(torch.randn(d_out // p, d_in // p, p, dtype=dtype, device=device) * std)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return bca(x, self.weight)
+
+    def extra_repr(self) -> str:
+        q_out, q_in, p = self.weight.shape
+        return f"d_in={q_in * p}, d_out={q_out * p}, p={p}"

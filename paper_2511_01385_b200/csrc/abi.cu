@@ -9,6 +9,7 @@
 
 #include "../../include/rdfft.h"
 #include "bca_v1.cuh"
+#include "bca_tiled.cuh"
 #include "kernels_v1.cuh"
 #include "plan2.cuh"
 #include "plan3.cuh"
@@ -145,6 +146,28 @@ int grid_for(K kernel, int threads, size_t smem, int64_t units) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * num_sms()));
 }
 
+
+int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, int q_out, int p, int logp, int dtype,
+                  cudaStream_t st) {
+  BcaTiledPlan plan{};
+  if (!bca_tiled_plan(false, false, T, q_in, q_out, p, num_sms(), &plan)) return RDFFT_E_SHAPE;
+  const dim3 grid((unsigned)std::min<int64_t>(plan.tiles, (int64_t)num_sms() * 4), (unsigned)plan.groups);
+  if (dtype == RDFFT_F32) {
+    auto k = bca_fwd_tiled_kernel<float>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
+                                                  static_cast<float*>(y), T, q_in, q_out, p, logp, plan.vt, plan.grp);
+  } else {
+    auto k = bca_fwd_tiled_kernel<__nv_bfloat16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const __nv_bfloat16*>(x),
+                                                  static_cast<const __nv_bfloat16*>(w),
+                                                  static_cast<__nv_bfloat16*>(y), T, q_in, q_out, p, logp, plan.vt,
+                                                  plan.grp);
+  }
+  return launched();
+}
+
 }  // namespace
 
 extern "C" {
@@ -177,9 +200,9 @@ int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int6
   if (overlap(y, T * d_out * s, x, T * d_in * s) || overlap(y, T * d_out * s, w, (size_t)q_out * q_in * p * s))
     return RDFFT_E_ALIAS;
   const size_t smem = bca_fwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
-  if (smem > 227 * 1024) return RDFFT_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logp = ilog2(p);
+  if (smem > 227 * 1024) return bca_fwd_tiled(x, w, y, T, q_in, q_out, (int)p, logp, dtype, st);
   const bool fast =
       dtype == RDFFT_F32
           ? bca_fwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w), static_cast<float*>(y), T,
@@ -223,12 +246,33 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
       overlap(dw, nw * 4, dx, xb))
     return RDFFT_E_ALIAS;
   const size_t smem = bca_bwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
-  if (smem > 227 * 1024) return RDFFT_E_SHAPE;
+  const bool tiled = smem > 227 * 1024;
+  BcaTiledPlan plan{};
+  if (tiled && !bca_tiled_plan(true, dx == g, T, q_in, q_out, (int)p, num_sms(), &plan)) return RDFFT_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(dw, 0, nw * sizeof(float), st) != cudaSuccess) return RDFFT_E_CUDA;
   const int logp = ilog2(p);
+  if (tiled && T > 0) {
+    const dim3 grid((unsigned)std::min<int64_t>(plan.tiles, (int64_t)num_sms() * 4), (unsigned)plan.groups);
+    if (dtype == RDFFT_F32) {
+      auto k = bca_bwd_tiled_kernel<float>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+      k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
+                                                    static_cast<const float*>(g), static_cast<float*>(dx), dw, T,
+                                                    q_in, q_out, (int)p, logp, plan.vt, plan.grp);
+    } else {
+      auto k = bca_bwd_tiled_kernel<__nv_bfloat16>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+      k<<<grid, kBcaTiledThreads, plan.smem, st>>>(
+          static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+          static_cast<const __nv_bfloat16*>(g), static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out, (int)p, logp,
+          plan.vt, plan.grp);
+    }
+    if ((rc = launched()) != RDFFT_OK) return rc;
+    return launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/true, st);
+  }
   const bool fast =
-      T > 0 && (dtype == RDFFT_F32
+      !tiled && T > 0 && (dtype == RDFFT_F32
                     ? bca_bwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w),
                                           static_cast<const float*>(g), static_cast<float*>(dx), dw, T, q_in, q_out,
                                           (int)p, num_sms(), st)
@@ -238,7 +282,7 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
                           (int)p, num_sms(), st));
   if (fast) {
     if ((rc = launched()) != RDFFT_OK) return rc;
-  } else if (T > 0) {
+  } else if (T > 0 && !tiled) {
     if (dtype == RDFFT_F32) {
       auto k = bca_bwd_v1_kernel<float>;
       const int grid = grid_for(k, kBcaThreads, smem, T);

@@ -1,0 +1,96 @@
+"""GPU: the autograd adapter against the float64 oracle, and its
+memory claim (Tab. 1): the fused layer allocates no spectra or other
+intermediates in forward, and backward needs only dw beyond grad_output."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as o
+from paper_2511_01385_b200 import bca as B
+from paper_2511_01385_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built(cuda_device):
+    from paper_2511_01385_b200 import build
+
+    build.build()
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("bf16", 2e-2)])
+@pytest.mark.parametrize("q_out,q_in,p", [(2, 2, 256), (4, 4, 1024), (2, 3, 64), (1, 2, 128)])
+def test_adapter_grads_match_oracle(q_out, q_in, p, dtype, tol):
+    T = 37
+    x, w, g = synth.bca_inputs(T, q_in * p, q_out * p, p, seed=7 + p, dtype=dtype)
+    layer = B.BlockCirculantAdapter(q_in * p, q_out * p, p, dtype=x.dtype, device="cuda")
+    with torch.no_grad():
+        layer.weight.copy_(w.cuda())
+    xc = x.cuda().requires_grad_(True)
+    y = layer(xc)
+    y.backward(g.cuda())
+    torch.cuda.synchronize()
+    xo, wo, go = f64(x), f64(w), f64(g)
+    assert rel(f64(y), o.bca_fwd(xo, wo)) <= tol
+    dxo, dwo = o.bca_bwd(xo, wo, go)
+    assert rel(f64(xc.grad), dxo) <= tol
+    assert layer.weight.grad.dtype == layer.weight.dtype
+    assert rel(f64(layer.weight.grad), dwo) <= tol
+
+
+def test_adapter_gradcheck_small():
+    # double precision is not a kernel dtype; check the chain rule numerically in fp32 instead
+    torch.manual_seed(0)
+    x = torch.randn(5, 64, device="cuda", requires_grad=True)
+    w = (torch.randn(2, 2, 32, device="cuda") * 0.2).requires_grad_(True)
+    loss = B.bca(x, w).square().sum()
+    loss.backward()
+    eps = 1e-2
+    for t, grad in ((x, x.grad), (w, w.grad)):
+        flat = t.detach().view(-1)
+        for i in (0, 7, flat.numel() - 1):
+            old = flat[i].item()
+            flat[i] = old + eps
+            lp = B.bca(x.detach(), w.detach()).square().sum().item()
+            flat[i] = old - eps
+            lm = B.bca(x.detach(), w.detach()).square().sum().item()
+            flat[i] = old
+            fd = (lp - lm) / (2 * eps)
+            assert abs(fd - grad.view(-1)[i].item()) <= 2e-2 * max(1.0, abs(fd))
+
+
+@pytest.mark.parametrize("B_,D,p", [(256, 4096, 1024), (256, 4096, 256), (16, 1024, 256)])
+def test_single_layer_peak_memory(B_, D, p):
+    """Tab. 1 setting: peak memory of one training step of one layer.
+
+    Beyond x, w and grad_output the fused path may allocate exactly y (forward)
+    and the fp32 dw (+ its cast for bf16 parameters) - no spectra, no complex
+    intermediates; dx reuses grad_output.  autograd's AccumulateGrad may
+    copy dx into x.grad because the caller still holds g: one more [B, D] block,
+    which is not the layer's."""
+    dt = torch.bfloat16
+    layer = B.BlockCirculantAdapter(D, D, p, dtype=dt, device="cuda")
+    x = torch.randn(B_, D, device="cuda", dtype=dt, requires_grad=True)
+    g = torch.randn(B_, D, device="cuda", dtype=dt)
+    torch.cuda.synchronize()
+    torch.cuda.reset_peak_memory_stats()
+    base = torch.cuda.memory_allocated()
+    y = layer(x)
+    y.backward(g)
+    torch.cuda.synchronize()
+    extra = torch.cuda.max_memory_allocated() - base
+    q = D // p
+    wbytes = q * q * p
+    allowed = 2 * B_ * D * 2 + wbytes * 4 + wbytes * 2  # y, x.grad copy, dw (fp32), dw cast to bf16
+    granule = 512 * 5  # caching-allocator rounding per block
+    assert extra <= allowed + granule, (extra, allowed)
+    assert x.grad.data_ptr() != 0

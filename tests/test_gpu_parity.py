@@ -199,7 +199,9 @@ def test_packed_mul_spec_examples(cuda_device):
 # ------------------------------------------------------------------ BCA layer
 # fused fast paths: square q <= 4 with p in {256, 512, 1024}; the rest exercises the generic kernels
 BCA_SHAPES = [(1, 1, 2), (1, 1, 4), (2, 3, 8), (4, 2, 16), (3, 3, 64), (1, 1, 256), (3, 3, 256), (4, 4, 256),
-              (2, 2, 512), (1, 1, 1024), (2, 2, 1024), (3, 3, 1024), (4, 4, 1024), (2, 1, 4096)]
+              (2, 2, 512), (1, 1, 1024), (2, 2, 1024), (3, 3, 1024), (4, 4, 1024), (2, 1, 4096),
+              # weight spectra larger than shared memory (Tab. 1 shapes): tiled kernels
+              (16, 16, 256), (8, 8, 512), (32, 32, 128), (12, 40, 64), (40, 12, 64)]
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -221,8 +223,8 @@ def test_bca_fwd_bwd_match_oracle(q_out, q_in, p, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_bca_bwd_dx_overwrites_g_in_place(dtype):
-    p, q = 256, 3
+@pytest.mark.parametrize("q,p", [(3, 256), (16, 256)])
+def test_bca_bwd_dx_overwrites_g_in_place(dtype, q, p):
     T = 50
     x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=3, dtype=dtype)
     xc, wc, gc = x.cuda(), w.cuda(), g.cuda()

@@ -8,7 +8,7 @@ import torch  # noqa: E402
 from paper_2511_01385_b200 import rdfft as R  # noqa: E402
 from paper_2511_01385_b200 import synth  # noqa: E402
 
-for (q, p, T) in [(4, 1024, 9), (3, 256, 11), (2, 512, 5)]:
+for (q, p, T) in [(4, 1024, 9), (3, 256, 11), (2, 512, 5), (16, 256, 5), (32, 128, 3)]:
     for dt in ["bf16", "f32"]:
         x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=1, dtype=dt, device="cuda")
         y = R.bca_fwd(x, w)
