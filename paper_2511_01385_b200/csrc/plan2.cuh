@@ -93,11 +93,13 @@ struct Plan2 {
   static constexpr int NT = VT * LPV;
   static constexpr int WSTR = R + 2;        // float2 per window (+16 B pad)
   static constexpr int NWIN = S / 2;        // windows per row (first half of the slots)
-  static constexpr int ROWA = ((NWIN * WSTR + 14 + 15) / 16) * 16;  // room for the row skew (<= 14)
+  static constexpr int ROWA = ((NWIN * WSTR + 14 + 15) / 16) * 16;  // room for the row skew (<= 14, even)
   static constexpr int HF = VT * ROWA + 16;  // float2 in one H region
   static constexpr int TWS = M + 2;         // twiddle row (one per k), padded: 16-byte pair loads, no conflicts
   static constexpr int TWF = LPV * TWS;
   static constexpr int CHV = N / 4;         // 16-byte H chunks per vector
+  static constexpr int DC0 = NT - 32;       // first thread of the warp whose lanes run the DC sets
+  static constexpr int NTT = NT;            // threads per CTA (Plan2o adds a dedicated DC warp)
   // staged rows are skewed by 64 bytes: the two vectors of a warp read complementary bank halves
   static constexpr int SROW = N + 64 / (int)sizeof(T);
   static constexpr int STAGE = VT * SROW * (int)sizeof(T);
@@ -106,11 +108,13 @@ struct Plan2 {
   static_assert(VT <= 32, "one DC-set lane per vector in the last warp");
   static_assert((VT * CHV) % NT == 0, "chunk mapping");
 
-  // Row skew (float2): 16 lanes of one vector (R = 32) or two vectors (R = 16) share a
-  // shared-memory phase in the last pass; the DC warp has one lane per vector.
-  __host__ __device__ static constexpr int skew(int v) {
-    return LPV == 16 ? 2 * (v & 7) : (v & 1) * 8 + ((v >> 1) & 3) * 2;
-  }
+  // Row skew (float2).  R = 32: a 16-lane shared-memory phase of the last pass holds 8
+  // consecutive k of each of the 2 interleaved vectors of a warp (see P2Roles), so the two sit
+  // 8 float2 apart.  R = 16 (vector-major lanes): a phase holds 8 k of 2 vectors, likewise.
+  // The low bits spread the DC warp (one lane per vector) over the banks.  Skews are even:
+  // window bases stay 16-byte aligned.
+  static constexpr bool kInterleave = (LPV == 16);
+  __host__ __device__ static constexpr int skew(int v) { return (v & 1) * 8 + ((v >> 1) & 3) * 2; }
   __host__ __device__ static constexpr int row(int v) { return v * ROWA + skew(v); }
   // float2 offset of logical half-pair index q (0 <= q < N/2) of vector v
   __host__ __device__ static constexpr int hidx(int v, int q) { return row(v) + (q / R) * WSTR + (q % R); }
@@ -142,14 +146,19 @@ struct P2Roles {
     h1 = H + P::row(v1) + w1 * P::WSTR;
     s1 = v1 * P::N + 2 * c1;
     s1s = v1 * P::SROW + 2 * c1;
-    v2 = lt / P::LPV;
-    k = 1 + lt % P::LPV;
+    // Last-pass lanes: the VPW = 32 / LPV vectors of a warp are interleaved (lane = VPW (k-1) + v),
+    // so each 16-lane half of a 128-bit twiddle load touches LPV / 2 distinct rows (128 B, one
+    // wavefront); with vector-major lanes both halves read the same 16 rows (4 wavefronts).
+    // (R = 16 keeps vector-major lanes: measured faster there.)
+    constexpr int VPW = P::kInterleave ? 32 / P::LPV : 1;
+    v2 = P::kInterleave ? (lt / 32) * VPW + (lt % VPW) : lt / P::LPV;
+    k = 1 + (P::kInterleave ? (lt % 32) / VPW : lt % P::LPV);
     ha = H + P::row(v2) + k;
     hm = H + P::row(v2) + (R - k);
     hmz = (k == R / 2) ? (H + P::row(v2) + R) : hm;
     twf = TWf + (k - 1) * P::TWS;
     twi = TWi + (k - 1) * P::TWS;
-    dv = lt - (P::NT - 32);
+    dv = lt - P::DC0;
     hd = H + P::row(dv < 0 ? 0 : dv);
     vq = (P::CHV < P::NT) ? lt / P::CHV : 0;
     tq = (P::CHV < P::NT) ? lt % P::CHV : lt;
@@ -411,7 +420,7 @@ struct P2Smem {  // [stage 0 .. NSTG-1][H][TW][bars]
 };
 
 template <typename P, bool kInv>
-__global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restrict__ x, int64_t batch) {
+__global__ void __launch_bounds__(P::NTT) rdfft2_kernel(typename P::elem* __restrict__ x, int64_t batch) {
   using T = typename P::elem;
   using L = P2Smem<P>;
   constexpr int VT = P::VT, N = P::N;
@@ -421,8 +430,8 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
   float2* TW = reinterpret_cast<float2*>(base + L::TW_OFF);
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
   const int tid = threadIdx.x;
-  p2_tables<P>(kInv ? nullptr : TW, kInv ? TW : nullptr, tid, P::NT);
-  if (!kInv) p2_zero_pads<P>(H, VT, tid, P::NT);
+  p2_tables<P>(kInv ? nullptr : TW, kInv ? TW : nullptr, tid, P::NTT);
+  if (!kInv) p2_zero_pads<P>(H, VT, tid, P::NTT);
   if (tid == 0) {
     for (int q = 0; q < (P::NSTG > 0 ? P::NSTG : 1); ++q) mbar_init(bar + q, 1);
     fence_mbar_init();
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(P::NT) rdfft2_kernel(typename P::elem* __restr
         p2_last_fwd<P>(r, nv);
         p2_dc_fwd<P>(r, nv);
         __syncthreads();
-        p2_store<P>(r, xt, nv);
+        if (P::NTT == P::NT || tid < P::NT) p2_store<P>(r, xt, nv);
       } else {
         p2_load<P>(r, st, nv, k65536);
         __syncthreads();
@@ -487,15 +496,15 @@ bool launch_plan2_dir(typename P::elem* x, int64_t batch, int sms, cudaStream_t 
   if (!per_sm) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NT, L::BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NTT, L::BYTES);
     if (per_sm < 1) per_sm = 1;
     if (verbose())
       std::fprintf(stderr, "[rdfft] plan2 n=%d R=%d VT=%d NSTG=%d inv=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N,
-                   P::R, P::VT, P::NSTG, (int)kInv, (size_t)L::BYTES, P::NT, per_sm);
+                   P::R, P::VT, P::NSTG, (int)kInv, (size_t)L::BYTES, P::NTT, per_sm);
   }
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
-  k<<<grid, P::NT, L::BYTES, st>>>(x, batch);
+  k<<<grid, P::NTT, L::BYTES, st>>>(x, batch);
   return true;
 }
 

@@ -11,6 +11,7 @@
 #pragma once
 
 #include "plan2.cuh"
+#include "plan2o.cuh"
 #include "small.cuh"
 
 namespace rdfft {
@@ -413,6 +414,21 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
 #define RDFFT_FWD_NSTG 1  // forward staging depth for n = 512 / 1024 (0 = pass 1 straight from HBM)
 #endif
 // Returns true when a specialised kernel was launched for (n, T).
+// bf16 inverse, n = 512/1024: the staged-read kernel (plan2o.cuh; measured 64 -> 70-76 % of HBM);
+// everything else plan2 (the plan2o forward and n <= 256 measured slower).  RDFFT_PLAN2O=0 forces plan2.
+template <typename T, int N, int R, int VT>
+bool launch_p2(T* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
+  if constexpr (sizeof(T) == 2 && N >= 512) {
+    static const bool use_o = [] {
+      const char* e = std::getenv("RDFFT_PLAN2O");
+      return !(e && *e == '0');
+    }();
+    if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, 1>>(x, batch, sms, st);
+  }
+  return launch_plan2<Plan2<T, N, R, VT, (N >= 512 ? RDFFT_FWD_NSTG : 2)>, Plan2<T, N, R, VT, (N >= 512 ? 1 : 2)>>(
+      x, batch, inverse, sms, st);
+}
+
 template <typename T>
 bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st) {
   (void)logn;
@@ -425,10 +441,10 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
     case 64:  // bf16 rows are 128 B (in-register path wins); fp32 rows (256 B) thrash L1 there
       if (sizeof(T) == 2) return launch_small<T, 64>(x, batch, inverse, sms, st);
       return launch_plan2<Plan2<T, 64, 16, 32>, Plan2<T, 64, 16, 32>>(x, batch, inverse, sms, st);
-    case 128: return launch_plan2<Plan2<T, 128, 16, 16>, Plan2<T, 128, 16, 16>>(x, batch, inverse, sms, st);
-    case 256: return launch_plan2<Plan2<T, 256, 16, 16>, Plan2<T, 256, 16, 16>>(x, batch, inverse, sms, st);
-    case 512: return launch_plan2<Plan2<T, 512, 32, 8, RDFFT_FWD_NSTG>, Plan2<T, 512, 32, 8, 1>>(x, batch, inverse, sms, st);
-    case 1024: return launch_plan2<Plan2<T, 1024, 32, 8, RDFFT_FWD_NSTG>, Plan2<T, 1024, 32, 8, 1>>(x, batch, inverse, sms, st);
+    case 128: return launch_p2<T, 128, 16, 16>(x, batch, inverse, sms, st);
+    case 256: return launch_p2<T, 256, 16, 16>(x, batch, inverse, sms, st);
+    case 512: return launch_p2<T, 512, 32, 8>(x, batch, inverse, sms, st);
+    case 1024: return launch_p2<T, 1024, 32, 8>(x, batch, inverse, sms, st);
     case 2048: return launch_plan3<Plan3<T, 2048, 4, 1>>(x, batch, inverse, sms, st);
     case 4096: return launch_plan3<Plan3<T, 4096, 2, 1>>(x, batch, inverse, sms, st);
     default: return false;
