@@ -57,6 +57,19 @@ struct sio<__nv_bfloat16> {
 };
 
 template <typename T>
+struct sio1;  // shared-memory single-element loads of T, widened to fp32
+template <>
+struct sio1<float> {
+  __device__ __forceinline__ static float ld(const float* p, uint32_t) { return *p; }
+};
+template <>
+struct sio1<__nv_bfloat16> {
+  __device__ __forceinline__ static float ld(const __nv_bfloat16* p, uint32_t k65536) {
+    return __uint_as_float((uint32_t)(*reinterpret_cast<const unsigned short*>(p)) * k65536);
+  }
+};
+
+template <typename T>
 struct gio;  // global pair loads / stores (streaming)
 template <>
 struct gio<float> {

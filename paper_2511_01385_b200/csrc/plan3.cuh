@@ -175,6 +175,55 @@ __device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2
   }
 }
 
+// Inverse last-pass set read straight from the staged tile (natural order, element type T): the
+// values p3_last_set<M, true> would read from H after the load phase copied them there.
+template <int M, typename T>
+__device__ __forceinline__ void p3_last_set_inv_st(const T* sa, const T* sm, float2* ha, float2* hmo, const float2* tw,
+                                                   int n, uint32_t k65536) {
+  constexpr int WS = 4 * 34, LM = ilog2c<M>();
+  float zr[M], zi[M];
+  ct::static_for<0, M / 2>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    zr[rev_bits<LM>(q)] = sio1<T>::ld(sa + q * 128, k65536);
+    zi[rev_bits<LM>(q + M / 2)] = -sio1<T>::ld(sa + q * 128 + n / 2, k65536);
+    zr[rev_bits<LM>(q + M / 2)] = sio1<T>::ld(sm + (M / 2 - 1 - q) * 128, k65536);
+    zi[rev_bits<LM>(q)] = sio1<T>::ld(sm + (M / 2 - 1 - q) * 128 + n / 2, k65536);
+  });
+  cfft_dit<M, true>(zr, zi);
+  ct::static_for<0, M>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    constexpr int rj = rev_bits<LM>(j);
+    const float2 t = tw[j * 64];
+    const float q = zr[rj];
+    zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
+    zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
+  });
+  ct::static_for<0, M / 2>([&](auto J) {
+    constexpr int jj = decltype(J)::value;
+    constexpr int r1 = rev_bits<LM>(jj), r2 = rev_bits<LM>(jj + M / 2);
+    ha[jj * WS] = make_float2(zr[r1], zr[r2]);
+    hmo[jj * WS] = make_float2(zi[r1], zi[r2]);
+  });
+}
+
+// Inverse last-pass DC set from the staged tile: slots j 128 and j 128 + n/2 -> H half pairs.
+template <int M, typename T>
+__device__ __forceinline__ void p3_dc_inv_st(const T* s, float2* hd, int n, uint32_t k65536) {
+  constexpr int WS = 4 * 34;
+  float d[M];
+  ct::static_for<0, M / 2>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    d[j] = sio1<T>::ld(s + j * 128, k65536);
+    d[j + M / 2] = sio1<T>::ld(s + j * 128 + n / 2, k65536);
+  });
+  rfft_inv_reg<M>(d);
+  const float sc = 1.0f / (float)n;
+  ct::static_for<0, M / 2>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    hd[j * WS] = make_float2(d[j] * sc, d[j + M / 2] * sc);
+  });
+}
+
 // DC set of a pass: M reals-pairs at stride WS (float2 lanes), real M-point FFT (unscaled inverse).
 template <int M, int WS, bool kInv, typename V>
 __device__ __forceinline__ void p3_dc_set(float2* hd, float scale) {
@@ -304,6 +353,16 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
     });
     if (dcl >= 0 && dcl < nv) p3_dc_set<P::M3, 4 * WS, kInv, float>(lhd, kInv ? 1.0f / N : 1.0f);
   };
+  auto last_inv_st = [&](const T* st, int nv) {  // the inverse's first pass, reading the staged tile
+    ct::static_for<0, LITEMS>([&](auto RR) {
+      constexpr int r = decltype(RR)::value;
+      constexpr int dv = r * LSTEP;
+      constexpr int off = dv * P::ROWA + 2 * dv;
+      const T* sv = st + (vl0 + dv) * N;
+      if (vl0 + dv < nv) p3_last_set_inv_st<P::M3, T>(sv + qa, sv + qm, lha + off, lhz + off, ltw, N, k65536);
+    });
+    if (dcl >= 0 && dcl < nv) p3_dc_inv_st<P::M3, T>(st + dcl * N, lhd, N, k65536);
+  };
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
@@ -343,19 +402,9 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
         }
       });
     } else {
-      ct::static_for<0, VT * P::CHV / NT>([&](auto RR) {  // load
-        constexpr int r = decltype(RR)::value;
-        constexpr int v = r / (P::CHV / NT), toff = NT * (r % (P::CHV / NT));
-        if (v < nv) {
-          const T* s = st + v * N + 2 * (tid + toff);
-          const float2 lo = sio<T>::ld2(s, k65536), hi = sio<T>::ld2(s + N / 2, k65536);
-          *reinterpret_cast<float4*>(hq + P::row(v) + (2 * toff / R) * WS) = make_float4(lo.x, hi.x, lo.y, hi.y);
-        }
-      });
+      last_inv_st(st, nv);  // reads the staged tile directly (no staged -> H copy)
       __syncthreads();
       if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
-      last(nv);
-      __syncthreads();
       middle(nv);
       __syncthreads();
       if (v1 < nv) {  // inverse pass 1
