@@ -283,15 +283,31 @@ def run_gpu(args):
     # ---- roofline for the dominant kernel (largest share of the step)
     kern_bytes = {"rdfft_fwd": bytes_fft, "rdfft_inv": bytes_fft, "packed_mul": 2 * n * s * batch,
                   "bca_fwd": T * (d_in + d_out) * s, "bca_bwd": T * (2 * d_in + d_out) * s}
+    # BCA is bound by FP32 issue, not HBM: algorithmic flops (the paper's radix-2 count
+    # F(p) per transform, 8 flops per complex multiply-add) against the FP32 FMA peak
+    # 148 SMs x 128 lanes x 2 flops x the SM clock (B200_PROFILING.md unit counts)
+    q_in, q_out = d_in // p, d_out // p
+    prod = q_out * q_in * (8 * (p // 2 - 1) + 4)
+    kern_flops = {"bca_fwd": T * ((q_in + q_out) * rfft_flops(p) + prod),
+                  "bca_bwd": T * ((2 * q_in + q_out) * rfft_flops(p) + 2 * prod)}
     rooflines = {}
     for k, b in kern_bytes.items():
         ach = b / (seg[k] * 1e-3) / 1e9
-        rooflines[k] = {"ms": seg[k], "achieved_GBps": ach, "frac": ach / hbm, "bytes": b}
+        rooflines[k] = {"ms": seg[k], "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "bytes": b, "achieved_GBps": ach}
+    clocks = sampler.summary()
+    fp32_peak = 148 * 128 * 2 * (clocks.get("sm_max_mhz") or 1965) * 1e6 / 1e12
+    for k, f in kern_flops.items():
+        ach = f / (seg[k] * 1e-3) / 1e12
+        rooflines[k].update({"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                             "frac": ach / fp32_peak, "flops": f,
+                             "hbm_frac": rooflines[k]["achieved_GBps"] / hbm})
     dom = max(kern_bytes, key=lambda k: seg[k])
     traffic = ncu_traffic(dom, batch)
-    roofline = {"kernel": dom, "bound": "hbm", "achieved": rooflines[dom]["achieved_GBps"], "peak": hbm,
-                "unit": "GB/s", "frac": rooflines[dom]["frac"], "traffic": traffic, "peak_source": peak_src,
-                "bytes_per_launch": kern_bytes[dom], "ms_per_launch": seg[dom]}
+    roofline = {"kernel": dom, "bound": rooflines[dom]["bound"], "achieved": rooflines[dom]["achieved"],
+                "peak": rooflines[dom]["peak"], "unit": rooflines[dom]["unit"], "frac": rooflines[dom]["frac"],
+                "traffic": traffic, "peak_source": peak_src, "bytes_per_launch": kern_bytes[dom],
+                "ms_per_launch": seg[dom]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -300,7 +316,6 @@ def run_gpu(args):
                "sample": f"float64 oracle rdfft_fwd+rdfft_inv on {done} seeded vectors of n={n} "
                          f"({t:.1f} s), same algorithmic-bytes unit"}
 
-    clocks = sampler.summary()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -322,6 +337,17 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def rfft_flops(n):
+    """Exact flop count of the paper's radix-2 real FFT: per stage m, each of the
+    n/2m blocks costs 2 (k = 0) + 10 per general four-slot group (complex multiply 6 + 4 adds);
+    the m = 1 stage is n/2 butterflies of 2 adds.  19 976 at n = 1024."""
+    total, m = n, 2
+    while m < n:
+        total += (n // (2 * m)) * (2 + 10 * (m // 2 - 1))
+        m *= 2
+    return total
 
 
 def ncu_traffic(kernel, batch):

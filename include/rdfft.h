@@ -104,6 +104,16 @@ int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int6
 int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
             int64_t d_out, int64_t p, int dtype, void* stream);
 
+/* bca_bwd_accum — bca_bwd that ADDS this call's weight gradient to dw instead of
+ * overwriting it (gradient accumulation over micro-batches; the paper trains
+ * with accumulation 4).  Same arguments, aliasing rules and dx as
+ * bca_bwd.  dw's old contents are first forward-transformed in place (fp32
+ * rdFFT, exact up to one round trip, ~1e-7 relative), the new spectra are
+ * accumulated on top and the usual in-place inverse finishes:
+ *   dw <- dw + IrdFFT( sum_t conj(X_tj) (.) G_ti ).                          */
+int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
+                  int64_t d_out, int64_t p, int dtype, void* stream);
+
 /* Static, never-allocating description of a status code. */
 const char* rdfft_status_str(int status);
 

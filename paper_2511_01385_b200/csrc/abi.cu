@@ -226,8 +226,8 @@ int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int6
   return launched();
 }
 
-int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in, int64_t d_out,
-            int64_t p, int dtype, void* stream) {
+static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
+                 int64_t d_out, int64_t p, int dtype, void* stream, bool accumulate) {
   int rc = bca_check(x, w, T, d_in, d_out, p, dtype);
   if (rc != RDFFT_OK) return rc;
   if (!dw) return RDFFT_E_NULL;
@@ -250,7 +250,12 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
   BcaTiledPlan plan{};
   if (tiled && !bca_tiled_plan(true, dx == g, T, q_in, q_out, (int)p, num_sms(), &plan)) return RDFFT_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(dw, 0, nw * sizeof(float), st) != cudaSuccess) return RDFFT_E_CUDA;
+  if (accumulate) {  // old dw -> its spectra; the kernels add theirs; the finalize inverse returns old + new
+    if ((rc = launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/false, st)) != RDFFT_OK)
+      return rc;
+  } else if (cudaMemsetAsync(dw, 0, nw * sizeof(float), st) != cudaSuccess) {
+    return RDFFT_E_CUDA;
+  }
   const int logp = ilog2(p);
   if (tiled && T > 0) {
     const dim3 grid((unsigned)std::min<int64_t>(plan.tiles, (int64_t)num_sms() * 4), (unsigned)plan.groups);
@@ -304,6 +309,16 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
   return launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/true, st);
 }
 
+int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in, int64_t d_out,
+            int64_t p, int dtype, void* stream) {
+  return bca_bwd_impl(x, w, g, dx, dw, T, d_in, d_out, p, dtype, stream, false);
+}
+
+int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
+                  int64_t d_out, int64_t p, int dtype, void* stream) {
+  return bca_bwd_impl(x, w, g, dx, dw, T, d_in, d_out, p, dtype, stream, true);
+}
+
 const char* rdfft_status_str(int status) {
   switch (status) {
     case RDFFT_OK: return "ok";
@@ -320,6 +335,6 @@ const char* rdfft_status_str(int status) {
 
 uint64_t rdfft_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int rdfft_abi_version(void) { return 100; }
+int rdfft_abi_version(void) { return 101; }
 
 }  // extern "C"

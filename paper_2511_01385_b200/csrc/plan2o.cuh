@@ -23,6 +23,10 @@ struct Plan2o : Plan2<__nv_bfloat16, N_, R_, VT_, NSTG_> {
   using B = Plan2<__nv_bfloat16, N_, R_, VT_, NSTG_>;
   static constexpr int DC0 = B::NT;          // the DC warp follows the last-pass warps
   static constexpr int NTT = B::NT + 32;     // threads per CTA
+  // Staged rows 12 words (24 bf16) apart mod 32 banks: the interleaved vector pair of a last-pass
+  // warp reads disjoint banks (8-9 words each), and so do the DC warp's 8 lanes (one per row).
+  static constexpr int SROW = B::N + 24;
+  static constexpr int STAGE = B::VT * SROW * 2;
 };
 
 __device__ __forceinline__ float bf16_at(const __nv_bfloat16* p, uint32_t k65536) {

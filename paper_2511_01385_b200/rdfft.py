@@ -43,8 +43,9 @@ def _lib():
         lib.rdfft_packed_conjmul.argtypes = [vp, vp, i64, i64, i64, i32, vp]
         lib.bca_fwd.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_bwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
+        lib.bca_bwd_accum.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
         for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
-                  "rdfft_abi_version"):
+                  "bca_bwd_accum", "rdfft_abi_version"):
             getattr(lib, f).restype = i32
         lib.rdfft_status_str.argtypes = [i32]
         lib.rdfft_status_str.restype = ctypes.c_char_p
@@ -54,7 +55,7 @@ def _lib():
 
 
 EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
-           "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
+           "bca_bwd_accum", "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
 
 
 def _ptr(t):
@@ -139,9 +140,10 @@ def bca_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None = None) -> 
 
 
 def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor | None = None,
-            dw: torch.Tensor | None = None):
+            dw: torch.Tensor | None = None, accumulate: bool = False):
     """(dx, dw) of the BCA layer for dL/dy = g.  dx may be g itself when d_in == d_out
-    (grad_output overwritten in place).  dw is fp32 [q_out, q_in, p]."""
+    (grad_output overwritten in place).  dw is fp32 [q_out, q_in, p]; with
+    accumulate=True (bca_bwd_accum) this call's gradient is added to dw's contents."""
     _check(x, "x")
     _check(w, "w")
     _check(g, "g")
@@ -150,13 +152,15 @@ def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor 
     if dx is None:
         dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
     if dw is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs the dw to add into")
         dw = torch.empty((q_out, q_in, p), dtype=torch.float32, device=x.device)
     _check(dx, "dx")
     _check(dw, "dw")
     if dw.dtype != torch.float32:
         raise ValueError("dw must be float32 (P:L486)")
-    _call("bca_bwd", _ptr(x), _ptr(w), _ptr(g), _ptr(dx), _ptr(dw), x.numel() // d_in, d_in, d_out, p,
-          _dtype(x), _stream(x))
+    _call("bca_bwd_accum" if accumulate else "bca_bwd", _ptr(x), _ptr(w), _ptr(g), _ptr(dx), _ptr(dw),
+          x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
     return dx, dw
 
 

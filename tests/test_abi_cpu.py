@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lib):
     from paper_2511_01385_b200 import rdfft
 
     assert set(rdfft.EXPORTS) == set(declared_functions())
-    assert lib.rdfft_abi_version() == 100
+    assert lib.rdfft_abi_version() == 101
 
 
 def test_status_strings(lib):
@@ -87,6 +87,10 @@ def test_bca_validation(lib):
     assert lib.bca_bwd(FAKE, FAKE2, g, FAKE, dw, 4, 768, 768, 256, 1, None) == 6   # dx overlaps x
     assert lib.bca_bwd(FAKE, FAKE2, g, dx, None, 4, 768, 768, 256, 1, None) == 2
     assert lib.bca_bwd(FAKE, FAKE2, g, dx, ctypes.c_void_p(0x70000010), 4, 768, 768, 256, 1, None) == 6
+    for f in (lib.bca_bwd, lib.bca_bwd_accum):  # the accumulate entry point validates identically
+        assert f(FAKE, FAKE2, g, g, dw, 4, 512, 768, 256, 1, None) == 6
+        assert f(FAKE, FAKE2, g, dx, None, 4, 768, 768, 256, 1, None) == 2
+        assert f(FAKE, FAKE2, g, dx, dw, 4, 768, 768, 100, 1, None) == 1
 
 
 def test_oracle_not_imported_by_product_path():

@@ -237,6 +237,28 @@ def test_bca_bwd_dx_overwrites_g_in_place(dtype, q, p):
     assert rel_l2_rows(f64(gc), dxo) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("q,p", [(3, 256), (4, 1024), (2, 64), (16, 256)])
+def test_bca_bwd_accumulate(dtype, q, p):
+    """bca_bwd_accum (N4): dw <- dw + this call's gradient; two micro-batches accumulate to the
+    full-batch gradient (linearity of Eq. 5 over tokens)."""
+    T = 40
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=11 + p, dtype=dtype)
+    xc, wc, gc = x.cuda(), w.cuda(), g.cuda()
+    dw0 = synth.randn((q, q, p), seed=5, dtype="f32").cuda()
+    dw = dw0.clone()
+    R.bca_bwd(xc[:17], wc, gc[:17].clone(), dw=dw, accumulate=True)
+    R.bca_bwd(xc[17:], wc, gc[17:].clone(), dw=dw, accumulate=True)
+    torch.cuda.synchronize()
+    _, dwo = o.bca_bwd(f64(x), f64(w), f64(g))
+    ref = dwo + f64(dw0)
+    assert rel_l2_rows(f64(dw).reshape(1, -1), ref.reshape(1, -1)) <= (1e-5 if dtype == "f32" else 2e-2)
+    empty = dw0.clone()
+    R.bca_bwd(xc[:0], wc, gc[:0], dw=empty, accumulate=True)  # no tokens: dw unchanged up to one round trip
+    torch.cuda.synchronize()
+    assert rel_l2_rows(f64(empty).reshape(1, -1), f64(dw0).reshape(1, -1)) <= 1e-6
+
+
 def test_bca_identity_and_shift(cuda_device):
     p, q = 64, 2
     w = torch.zeros(q, q, p)

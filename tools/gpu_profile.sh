@@ -10,7 +10,7 @@ python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $OUT/launches_bench.log 2>&1
 i=0
-for K in "rdfft2_kernel.*bfloat16.*bool.0" "rdfft2_kernel.*bfloat16.*bool.1" "packed_mul" "bca_fwd" "bca_bwd"; do
+for K in "rdfft2_kernel.*bfloat16.*bool.0" "rdfft2o_inv_kernel.*1024" "packed_mul" "bca_fwd" "bca_bwd"; do
   i=$((i+1))
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$K" -s 1 -c 1 \
       -o $OUT/prof_$i python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --batch 262144 > $OUT/ncu_$i.log 2>&1

@@ -61,6 +61,8 @@ def short(name):
 
 
 def family(name):
+    if "rdfft2o_inv_kernel" in name:
+        return "rdfft_inv"
     if "rdfft2_kernel" in name:
         return "rdfft_inv" if re.search(r",\s*(?:true|\(bool\)1|1)>\s*\(", name) else "rdfft_fwd"
     for k, f in [("bca_fwd", "bca_fwd"), ("bca_bwd", "bca_bwd"), ("packed_mul", "packed_mul"),
