@@ -32,7 +32,9 @@ struct Plan3 {
   static constexpr int WPV = N / (2 * W2);   // middle-pass windows per vector (first half)
   static constexpr int MIPV = WPV * KM;      // middle general items per vector
   static constexpr int KL = W2 / 2;          // last-pass lanes per vector (k = 1 .. 64)
-  static constexpr int TWM = M2 * KM, TWL = M3 * KL;
+  // last-pass twiddles W_N^{k r}, r = rev(j) = 4a + b: table of W_N^{4 k a} (a < M3/4), times W_N^{k b}
+  // (b < 4) held in registers -> 4 KB instead of 16 KB at n = 4096 (4 CTAs/SM instead of 3)
+  static constexpr int TWM = M2 * KM, TWL = (M3 / 4) * KL;
   static constexpr int CHV = N / 4;
   static constexpr int STAGE = VT * N * (int)sizeof(T);
   static_assert(M3 >= 4 && M3 <= 32, "plan3 shape");
@@ -123,9 +125,26 @@ __device__ __forceinline__ void p3_mid_set(float2* ha, float2* hm, const float2*
   }
 }
 
+// Last-pass twiddles of one lane k: W_N^{k r} = h[(r >> 2) 64] * w[r & 3] (w[0] = 1, not stored).
+struct LTw {
+  const float2* h;
+  float2 w1, w2, w3;
+  template <int R_>
+  __device__ __forceinline__ float2 at() const {
+    constexpr int a = R_ >> 2, b = R_ & 3;
+    const float2 t = h[a * 64];
+    if constexpr (b == 0) {
+      return t;
+    } else {
+      const float2 w = b == 1 ? w1 : (b == 2 ? w2 : w3);
+      return make_float2(fmaf(t.x, w.x, -t.y * w.y), fmaf(t.x, w.y, t.y * w.x));
+    }
+  }
+};
+
 // Last-pass general set: S_k = {j 128 +- k}, M3 blocks, half pairs hold (Z_j, Z_{j + M3/2}).
 template <int M, bool kInv>
-__device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2* hmi, float2* hmo, const float2* tw) {
+__device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2* hmi, float2* hmo, const LTw& tw) {
   constexpr int WS = 4 * 34, LM = ilog2c<M>();  // 128 slots = 4 padded windows
   float zr[M], zi[M];
   if (!kInv) {
@@ -137,7 +156,7 @@ __device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2
     });
     ct::static_for<1, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
-      const float2 t = tw[j * 64];
+      const float2 t = tw.template at<rev_bits<LM>(j)>();
       const float q = zr[j];
       zr[j] = fmaf(q, t.x, -zi[j] * t.y);
       zi[j] = fmaf(q, t.y, zi[j] * t.x);
@@ -161,7 +180,7 @@ __device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2
     ct::static_for<0, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
       constexpr int rj = rev_bits<LM>(j);
-      const float2 t = tw[j * 64];
+      const float2 t = tw.template at<rj>();
       const float q = zr[rj];
       zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
       zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
@@ -178,7 +197,7 @@ __device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2
 // Inverse last-pass set read straight from the staged tile (natural order, element type T): the
 // values p3_last_set<M, true> would read from H after the load phase copied them there.
 template <int M, typename T>
-__device__ __forceinline__ void p3_last_set_inv_st(const T* sa, const T* sm, float2* ha, float2* hmo, const float2* tw,
+__device__ __forceinline__ void p3_last_set_inv_st(const T* sa, const T* sm, float2* ha, float2* hmo, const LTw& tw,
                                                    int n, uint32_t k65536) {
   constexpr int WS = 4 * 34, LM = ilog2c<M>();
   float zr[M], zi[M];
@@ -193,7 +212,7 @@ __device__ __forceinline__ void p3_last_set_inv_st(const T* sa, const T* sm, flo
   ct::static_for<0, M>([&](auto J) {
     constexpr int j = decltype(J)::value;
     constexpr int rj = rev_bits<LM>(j);
-    const float2 t = tw[j * 64];
+    const float2 t = tw.template at<rj>();
     const float q = zr[rj];
     zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
     zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
@@ -265,17 +284,17 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
   float2* TWl = reinterpret_cast<float2*>(base + L::TWL_OFF);
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
   const int tid = threadIdx.x;
-  // tables: TWm[j 16 + k-1] = W_128^{k rev2(j)}, TWl[j 64 + k-1] = W_N^{k rev(j)}; inverse: conj (and 1/N on TWl)
+  // tables: TWm[j 16 + k-1] = W_128^{k rev2(j)}; TWl (see Plan3::TWL); inverse: conj (and 1/N on TWl)
   for (int e = tid; e < P::TWM; e += NT) {
     const int j = e / 16, k = 1 + e % 16;
     float s, c;
     sincospif(2.0f * (float)(k * rev_bits<2>(j)) / 128.0f, &s, &c);
     TWm[e] = kInv ? make_float2(c, s) : make_float2(c, -s);
   }
-  for (int e = tid; e < P::TWL; e += NT) {
-    const int j = e / 64, k = 1 + e % 64;
+  for (int e = tid; e < P::TWL; e += NT) {  // TWl[a 64 + k-1] = W_N^{4 k a} (inverse: conj / N)
+    const int a = e / 64, k = 1 + e % 64;
     float s, c;
-    sincospif(2.0f * (float)(k * rev_bits<P::LM3>(j)) / (float)N, &s, &c);
+    sincospif(2.0f * (float)(4 * k * a) / (float)N, &s, &c);
     TWl[e] = kInv ? make_float2(c * (1.0f / N), s * (1.0f / N)) : make_float2(c, -s);
   }
   for (int e = tid; e < P::NWIN * VT; e += NT) {  // window pads (zero imaginary inputs)
@@ -311,7 +330,18 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
   float2* lha = H + P::row(vl0) + P::pos(qa);
   float2* lhm = H + P::row(vl0) + P::pos(qm);
   float2* lhz = (kl == P::KL) ? (H + P::row(vl0) + P::pos(qa) + (R - (qa % R))) : lhm;
-  const float2* ltw = TWl + (kl - 1);
+  LTw ltw;
+  ltw.h = TWl + (kl - 1);
+  {
+    float s1, c1, s2, c2, s3, c3;
+    sincospif(2.0f * (float)kl / (float)N, &s1, &c1);
+    sincospif(4.0f * (float)kl / (float)N, &s2, &c2);
+    sincospif(6.0f * (float)kl / (float)N, &s3, &c3);
+    const float sg = kInv ? 1.0f : -1.0f;
+    ltw.w1 = make_float2(c1, sg * s1);
+    ltw.w2 = make_float2(c2, sg * s2);
+    ltw.w3 = make_float2(c3, sg * s3);
+  }
   constexpr int LSTEP = NT / P::KL;
   constexpr int LITEMS = VT * P::KL / NT;
   const int dcl = tid - (NT - VT);  // last DC: one lane per vector on the last threads
