@@ -11,9 +11,7 @@
 #include "bca_v1.cuh"
 #include "bca_tiled.cuh"
 #include "kernels_v1.cuh"
-#include "plan2.cuh"
-#include "plan3.cuh"
-#include "bca2.cuh"
+#include "fast.h"
 
 using namespace rdfft;
 

@@ -1,0 +1,18 @@
+// fast.h — declarations of the specialised launchers, each explicitly instantiated in its
+// own translation unit (tu_*.cu) so the library compiles in parallel.  Host-only interface.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rdfft {
+// plan3.cuh: specialised rdFFT kernels for every n in [2, 4096]; false if none applies.
+template <typename T>
+bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st);
+// bca2.cuh: fused BCA fast paths (square layers, q <= 4, p in {256, 512, 1024}).
+template <typename T>
+bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st);
+template <typename T>
+bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
+                  int sms, cudaStream_t st);
+}  // namespace rdfft

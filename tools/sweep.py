@@ -35,7 +35,9 @@ def main():
     ap.add_argument("--batch", type=int, default=1 << 20)
     a = ap.parse_args()
     build.build()
-    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+    from bench import peaks
+
+    peak = peaks()[0]
     for dt in a.dtypes.split(","):
         for n in map(int, a.ns.split(",")):
             batch = a.batch
