@@ -47,8 +47,22 @@ __device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 c) {  // c + a
 __device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 c) {  // c + conj(a) b
   return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(-a.y, b.x, c.y)));
 }
-__device__ __forceinline__ float2 rfma(float2 a, float2 b, float2 c) {  // componentwise c + a b
-  return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+
+// Branch-free per-bin multiply-accumulate shared by generic and special items.  The right
+// operand b is prepared once (per token) into four values so that every (i, j) pair costs
+// exactly 4 FFMA whether the bin pair is complex (c += a b or c += conj(a) b) or the special
+// (DC, Nyquist) pair of real bins (c.x += a.x b.x, c.y += a.y b.y):
+//   c.x += a.x p + a.y r,   c.y += a.x t + a.y u.
+struct PrepB {
+  float p, r, t, u;
+};
+template <bool kConjA>
+__device__ __forceinline__ PrepB prep_b(float2 b, bool special) {
+  if (special) return {b.x, 0.f, 0.f, b.y};
+  return kConjA ? PrepB{b.x, b.y, b.y, -b.x} : PrepB{b.x, -b.y, b.y, b.x};
+}
+__device__ __forceinline__ float2 pmac(float2 a, const PrepB& b, float2 c) {
+  return make_float2(fmaf(a.y, b.r, fmaf(a.x, b.p, c.x)), fmaf(a.y, b.u, fmaf(a.x, b.t, c.y)));
 }
 
 // Gather the two bins of item u from the half pairs at positions (pa, pb) of one row.
@@ -97,10 +111,15 @@ __device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int
       for (int j = 0; j < Q; ++j)
         if (i < q && j < q) w[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
     for (int tt = ts; tt < ntok; tt += TS) {
-      BinPair x[Q];
+      PrepB x1[Q];
+      float2 x2[Q];
 #pragma unroll
       for (int j = 0; j < Q; ++j)
-        if (j < q) x[j] = bins_get(H + P::row(tt * q + j), oa, ob, special);
+        if (j < q) {
+          const BinPair xb = bins_get(H + P::row(tt * q + j), oa, ob, special);
+          x1[j] = prep_b<false>(xb.b1, special);
+          x2[j] = xb.b2;
+        }
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
         if (i < q) {
@@ -108,8 +127,8 @@ __device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int
 #pragma unroll
           for (int j = 0; j < Q; ++j) {
             if (j < q) {
-              y.b1 = special ? rfma(w[i][j].b1, x[j].b1, y.b1) : cfma(w[i][j].b1, x[j].b1, y.b1);
-              y.b2 = cfma(w[i][j].b2, x[j].b2, y.b2);
+              y.b1 = pmac(w[i][j].b1, x1[j], y.b1);
+              y.b2 = cfma(w[i][j].b2, x2[j], y.b2);
             }
           }
           bins_put(H + P::row(tt * q + i), oa, ob, special, y);
@@ -328,13 +347,16 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
             xv[j] = bins_get(Hx + P::row(tt * q + j), oa, ob, special);
             gv[j] = bins_get(Hg + P::row(tt * q + j), oa, ob, special);
           }
+        PrepB g1[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+          if (i < q) g1[i] = prep_b<true>(gv[i].b1, special);
 #pragma unroll
         for (int i = 0; i < Q; ++i)
 #pragma unroll
           for (int j = 0; j < Q; ++j)
             if (i < q && j < q) {
-              acc[a][i][j].b1 = special ? rfma(xv[j].b1, gv[i].b1, acc[a][i][j].b1)
-                                        : cfmac(xv[j].b1, gv[i].b1, acc[a][i][j].b1);
+              acc[a][i][j].b1 = pmac(xv[j].b1, g1[i], acc[a][i][j].b1);
               acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
             }
 #pragma unroll
@@ -344,7 +366,7 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
 #pragma unroll
             for (int i = 0; i < Q; ++i)
               if (i < q) {
-                d.b1 = special ? rfma(wv[i][j].b1, gv[i].b1, d.b1) : cfmac(wv[i][j].b1, gv[i].b1, d.b1);
+                d.b1 = pmac(wv[i][j].b1, g1[i], d.b1);
                 d.b2 = cfmac(wv[i][j].b2, gv[i].b2, d.b2);
               }
             bins_put(Hx + P::row(tt * q + j), oa, ob, special, d);
@@ -504,13 +526,16 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
             xv[j] = bins_get(Hx + P::row(tt * q + j), oa, ob, special);
             gv[j] = bins_get(Hg + P::row(tt * q + j), oa, ob, special);
           }
+        PrepB g1[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+          if (i < q) g1[i] = prep_b<true>(gv[i].b1, special);
 #pragma unroll
         for (int i = 0; i < Q; ++i)
 #pragma unroll
           for (int j = 0; j < Q; ++j)
             if (i < q && j < q) {
-              acc[a][i][j].b1 = special ? rfma(xv[j].b1, gv[i].b1, acc[a][i][j].b1)
-                                        : cfmac(xv[j].b1, gv[i].b1, acc[a][i][j].b1);
+              acc[a][i][j].b1 = pmac(xv[j].b1, g1[i], acc[a][i][j].b1);
               acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
             }
 #pragma unroll
@@ -520,7 +545,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
 #pragma unroll
             for (int i = 0; i < Q; ++i)
               if (i < q) {
-                d.b1 = special ? rfma(wv[i][j].b1, gv[i].b1, d.b1) : cfmac(wv[i][j].b1, gv[i].b1, d.b1);
+                d.b1 = pmac(wv[i][j].b1, g1[i], d.b1);
                 d.b2 = cfmac(wv[i][j].b2, gv[i].b2, d.b2);
               }
             bins_put(Hx + P::row(tt * q + j), oa, ob, special, d);
@@ -599,24 +624,6 @@ bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const
   return true;
 }
 
-#ifndef RDFFT_BCA_FWD_VT
-#define RDFFT_BCA_FWD_VT 16   // p = 1024 forward: 32 vectors (8 tokens of q = 4) per tile, 512 threads
-#endif
-#ifndef RDFFT_BCA_FWD_NSTG
-#define RDFFT_BCA_FWD_NSTG 2  // ... with pass 1 reading x straight from HBM (H + W fill shared memory)
-#endif
-// Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
-template <typename T, int Q>
-bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st) {
-  switch (p) {
-    case 256: return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
-    case 1024:
-      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
-          x, w, y, T_, sms, st);
-    default: return false;
-  }
-}
 template <typename T, int Q>
 bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
                     cudaStream_t st) {
@@ -624,18 +631,6 @@ bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_
     case 256: return launch_bca_bwd2<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
     case 512: return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st);
     case 1024: return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-    default: return false;
-  }
-}
-
-template <typename T>
-bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
-  if (q_in != q_out) return false;
-  switch (q_in) {
-    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st);
-    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st);
-    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st);
-    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st);
     default: return false;
   }
 }
