@@ -624,28 +624,4 @@ bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const
   return true;
 }
 
-template <typename T, int Q>
-bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
-                    cudaStream_t st) {
-  switch (p) {
-    case 256: return launch_bca_bwd2<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-    case 512: return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st);
-    case 1024: return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-    default: return false;
-  }
-}
-
-template <typename T>
-bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
-                  int sms, cudaStream_t st) {
-  if (q_in != q_out) return false;
-  switch (q_in) {
-    case 1: return bca_bwd_fast_q<T, 1>(x, w, g, dx, dw, T_, p, sms, st);
-    case 2: return bca_bwd_fast_q<T, 2>(x, w, g, dx, dw, T_, p, sms, st);
-    case 3: return bca_bwd_fast_q<T, 3>(x, w, g, dx, dw, T_, p, sms, st);
-    case 4: return bca_bwd_fast_q<T, 4>(x, w, g, dx, dw, T_, p, sms, st);
-    default: return false;
-  }
-}
-
 }  // namespace rdfft
