@@ -114,6 +114,34 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
 int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
                   int64_t d_out, int64_t p, int dtype, void* stream);
 
+/* ---- packed-spectrum utilities ---------------------------
+ * rdfft_decode — the explicit decode step of the paper's Limitations
+ * ("explicit complex access needs a decode step that breaks the
+ * in-place property").  Out of place:
+ *   p: [batch][n] packed spectra (read only)
+ *   c: [batch][n + 2] interleaved bins (Re y_k, Im y_k), k = 0 .. n/2 — the
+ *      torch.fft.rfft layout; Im y_0 = Im y_{n/2} = 0 are written explicitly.
+ *   c may not overlap p (RDFFT_E_ALIAS).  Exact (a permutation).            */
+int rdfft_decode(const void* p, void* c, int64_t batch, int64_t n, int dtype, void* stream);
+
+/* rdfft_encode — inverse of rdfft_decode: c [batch][n + 2] -> p [batch][n]
+ * packed.  Im y_0 and Im y_{n/2} are ignored (zero for the
+ * spectrum of a real signal, Thm 1; not checked).  No overlap.   */
+int rdfft_encode(const void* c, void* p, int64_t batch, int64_t n, int dtype, void* stream);
+
+/* rdfft_packed_conj — a <- conj(a) per bin, in place (the conjugate of a
+ * Hermitian spectrum stays Hermitian): slots n/2+1 .. n-1 (the
+ * imaginary parts) change sign; exact.                              */
+int rdfft_packed_conj(void* a, int64_t batch, int64_t n, int dtype, void* stream);
+
+/* rdfft_packed_axpy — y <- y + alpha x, in the packed domain (the packing is
+ * linear, so this is the spectral axpy; alpha = -lr gives a spectral-domain
+ * SGD step).  y: [batch][n] in/out; x: [x_batch][n] read only,
+ * x_batch == 1 broadcasts.  fp32 FMA; bf16 results rounded to nearest even.
+ * x may not overlap y unless x == y and x_batch == batch.                   */
+int rdfft_packed_axpy(void* y, const void* x, float alpha, int64_t batch, int64_t n, int64_t x_batch, int dtype,
+                      void* stream);
+
 /* Static, never-allocating description of a status code. */
 const char* rdfft_status_str(int status);
 

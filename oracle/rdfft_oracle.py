@@ -39,6 +39,10 @@ __all__ = [
     "rdfft_inv",
     "packed_mul",
     "packed_conjmul",
+    "decode",
+    "encode",
+    "packed_conj",
+    "packed_axpy",
     "circulant",
     "block_circulant",
     "bca_fwd",
@@ -163,6 +167,38 @@ def packed_conjmul(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     """a (.) conj(b) per bin in the packed domain  (Eq. 5 conj products)."""
     n = np.shape(a)[-1]
     return pack((unpack(a) * np.conj(unpack(b)))[..., : n // 2 + 1], n)
+
+
+def decode(p: np.ndarray) -> np.ndarray:
+    """Explicit spectrum of a packed row as interleaved reals (Re y_0, Im y_0, ..., Re y_{n/2},
+    Im y_{n/2}), [..., n + 2] — the decode step of the Limitations into the rFFT
+    layout of P:L108-110 (n/2 + 1 complex bins).  Bins come from unpack."""
+    p = np.asarray(p, dtype=np.float64)
+    n = p.shape[-1]
+    Y = unpack(p)[..., : n // 2 + 1]
+    out = np.empty(p.shape[:-1] + (n + 2,), dtype=np.float64)
+    out[..., 0::2] = Y.real
+    out[..., 1::2] = Y.imag
+    return out
+
+
+def encode(c: np.ndarray) -> np.ndarray:
+    """Packed layout of interleaved bins [..., n + 2]; Im y_0, Im y_{n/2} ignored."""
+    c = np.asarray(c, dtype=np.float64)
+    n = c.shape[-1] - 2
+    return pack(c[..., 0::2] + 1j * c[..., 1::2], n)
+
+
+def packed_conj(p: np.ndarray) -> np.ndarray:
+    """conj(y_k) for every bin, in the packed layout (P:L290-293 closure; Thm 1)."""
+    n = np.shape(p)[-1]
+    return pack(np.conj(unpack(p))[..., : n // 2 + 1], n)
+
+
+def packed_axpy(y: np.ndarray, x: np.ndarray, alpha: float) -> np.ndarray:
+    """y + alpha x per bin, in the packed layout (spectral axpy / SGD step)."""
+    n = np.shape(y)[-1]
+    return pack((unpack(y) + alpha * unpack(x))[..., : n // 2 + 1], n)
 
 
 def circulant(c: np.ndarray) -> np.ndarray:

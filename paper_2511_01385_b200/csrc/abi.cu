@@ -166,9 +166,78 @@ int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, in
   return launched();
 }
 
+// shared validation of the packed-spectrum utilities: 1 = proceed, 0 = no-op, < 0 = -status
+int util_check(const void* a, const void* b, int64_t batch, int64_t n, int dtype) {
+  if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return -RDFFT_E_DTYPE;
+  if (!pow2_in_range(n)) return -RDFFT_E_SIZE;
+  if (batch < 0) return -RDFFT_E_SHAPE;
+  if (batch == 0) return 0;
+  if (!a || !b) return -RDFFT_E_NULL;
+  if (!aligned16(a) || !aligned16(b)) return -RDFFT_E_ALIGN;
+  return 1;
+}
+
 }  // namespace
 
 extern "C" {
+
+int rdfft_decode(const void* p, void* c, int64_t batch, int64_t n, int dtype, void* stream) {
+  const int ok = util_check(p, c, batch, n, dtype);
+  if (ok <= 0) return -ok;
+  const size_t s = dsize(dtype);
+  if (overlap(p, batch * n * s, c, batch * (n + 2) * s)) return RDFFT_E_ALIAS;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == RDFFT_F32)
+    launch_decode<float>(static_cast<const float*>(p), static_cast<float*>(c), batch, (int)n, num_sms(), st);
+  else
+    launch_decode<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(p), static_cast<__nv_bfloat16*>(c), batch,
+                                 (int)n, num_sms(), st);
+  return launched();
+}
+
+int rdfft_encode(const void* c, void* p, int64_t batch, int64_t n, int dtype, void* stream) {
+  const int ok = util_check(c, p, batch, n, dtype);
+  if (ok <= 0) return -ok;
+  const size_t s = dsize(dtype);
+  if (overlap(p, batch * n * s, c, batch * (n + 2) * s)) return RDFFT_E_ALIAS;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == RDFFT_F32)
+    launch_encode<float>(static_cast<const float*>(c), static_cast<float*>(p), batch, (int)n, num_sms(), st);
+  else
+    launch_encode<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(c), static_cast<__nv_bfloat16*>(p), batch,
+                                 (int)n, num_sms(), st);
+  return launched();
+}
+
+int rdfft_packed_conj(void* a, int64_t batch, int64_t n, int dtype, void* stream) {
+  const int ok = util_check(a, a, batch, n, dtype);
+  if (ok <= 0) return -ok;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == RDFFT_F32)
+    launch_packed_conj<float>(static_cast<float*>(a), batch, (int)n, ilog2(n), num_sms(), st);
+  else
+    launch_packed_conj<__nv_bfloat16>(static_cast<__nv_bfloat16*>(a), batch, (int)n, ilog2(n), num_sms(), st);
+  return launched();
+}
+
+int rdfft_packed_axpy(void* y, const void* x, float alpha, int64_t batch, int64_t n, int64_t x_batch, int dtype,
+                      void* stream) {
+  const int ok = util_check(y, x, batch, n, dtype);
+  if (ok < 0) return -ok;
+  if (x_batch < 0 || (batch > 0 && x_batch != 1 && x_batch != batch)) return RDFFT_E_SHAPE;
+  if (ok == 0) return RDFFT_OK;
+  const size_t s = dsize(dtype);
+  if (overlap(y, batch * n * s, x, x_batch * n * s) && !(y == x && x_batch == batch)) return RDFFT_E_ALIAS;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool bcast = x_batch == 1 && batch > 1;
+  if (dtype == RDFFT_F32)
+    launch_packed_axpy<float>(static_cast<float*>(y), static_cast<const float*>(x), alpha, batch, (int)n, bcast,
+                              num_sms(), st);
+  else
+    launch_packed_axpy<__nv_bfloat16>(static_cast<__nv_bfloat16*>(y), static_cast<const __nv_bfloat16*>(x), alpha,
+                                      batch, (int)n, bcast, num_sms(), st);
+  return launched();
+}
 
 int rdfft_fwd(void* x, int64_t batch, int64_t n, int dtype, void* stream) {
   return transform(x, batch, n, dtype, stream, false);
@@ -333,6 +402,6 @@ const char* rdfft_status_str(int status) {
 
 uint64_t rdfft_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int rdfft_abi_version(void) { return 101; }
+int rdfft_abi_version(void) { return 102; }
 
 }  // extern "C"

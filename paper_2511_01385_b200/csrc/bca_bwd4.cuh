@@ -210,10 +210,10 @@ inline bool use_bwd4() {
 template <typename T, int Q>
 bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
                     cudaStream_t st) {
-  const bool v4 = use_bwd4();
+  const bool v4 = use_bwd4() && Q % 2 == 0;  // odd q: half the pair-split product is predicated off
   switch (p) {
     case 256:  // odd q predicates half of the pair-split product: the 2-group kernel measured faster
-      if (v4 && Q % 2 == 0) return launch_bca_bwd4<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+      if (v4) return launch_bca_bwd4<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
       return launch_bca_bwd2<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
     case 512:
       if (v4) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);

@@ -15,4 +15,13 @@ bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out,
 template <typename T>
 bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
                   int sms, cudaStream_t st);
+// utils.cu: packed-spectrum utilities
+template <typename T>
+void launch_packed_conj(T* a, int64_t batch, int n, int logn, int sms, cudaStream_t st);
+template <typename T>
+void launch_packed_axpy(T* y, const T* x, float alpha, int64_t batch, int n, bool bcast, int sms, cudaStream_t st);
+template <typename T>
+void launch_decode(const T* p, T* c, int64_t batch, int n, int sms, cudaStream_t st);
+template <typename T>
+void launch_encode(const T* c, T* p, int64_t batch, int n, int sms, cudaStream_t st);
 }  // namespace rdfft

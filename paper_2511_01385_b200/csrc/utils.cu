@@ -1,0 +1,232 @@
+// utils.cu — packed-spectrum utilities: decode / encode between the packed
+// layout and the interleaved rFFT layout, conjugation and axpy in the packed
+// domain.  Memory-bound elementwise kernels: each element is read once and written once with
+// 16-byte (conj, axpy) or pair (decode, encode) accesses; grid-stride persistent grids.
+//
+//  * decode (the "decode step" of the Limitations): packed row p[n] ->
+//    c[n + 2] = (Re y_0, Im y_0, ..., Re y_{n/2}, Im y_{n/2}) with Im y_0 = Im y_{n/2} = 0.
+//  * encode: the inverse map (Im y_0, Im y_{n/2} are ignored: zero for a Hermitian spectrum).
+//  * conj:  y_k -> conj(y_k) is a sign flip of slots n/2 + 1 .. n - 1 (a bit operation, exact).
+//  * axpy:  y <- y + alpha x; the packing is linear, so this is the spectral-domain axpy
+//    (and, with alpha = -lr, a spectral-domain SGD step).
+#include "common.cuh"
+#include "fast.h"
+
+namespace rdfft {
+
+namespace {
+
+constexpr int kUThreads = 256;
+
+template <typename T>
+struct vec16;  // 16-byte vector of T as raw words
+template <>
+struct vec16<float> {
+  static constexpr int E = 4;
+};
+template <>
+struct vec16<__nv_bfloat16> {
+  static constexpr int E = 8;
+};
+
+// sign-flip mask of element `col` (bits of one T)
+template <typename T>
+__device__ __forceinline__ uint32_t neg_bit(int col, int n) {
+  return col > n / 2 ? (sizeof(T) == 4 ? 0x80000000u : 0x8000u) : 0u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kUThreads) packed_conj_kernel(T* __restrict__ a, int64_t total, int n, int logn) {
+  constexpr int E = vec16<T>::E;
+  const int64_t nvec = total / E;
+  uint4* a4 = reinterpret_cast<uint4*>(a);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = v * E;  // a vector may span several rows when n < E
+    uint4 u = __ldcs(a4 + v);
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (sizeof(T) == 4) {
+        w[i] ^= neg_bit<T>((int)((e0 + i) & (n - 1)), n);
+      } else {
+        w[i] ^= neg_bit<T>((int)((e0 + 2 * i) & (n - 1)), n) | (neg_bit<T>((int)((e0 + 2 * i + 1) & (n - 1)), n) << 16);
+      }
+    }
+    __stcs(a4 + v, make_uint4(w[0], w[1], w[2], w[3]));
+  }
+  // ragged tail (total % E elements; only when n < E, i.e. tiny rows)
+  for (int64_t e = nvec * E + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(e & (n - 1));
+    if (col > n / 2) {
+      if constexpr (sizeof(T) == 4)
+        a[e] = -a[e];
+      else
+        a[e] = __hneg(a[e]);
+    }
+  }
+  (void)logn;
+}
+
+template <typename T>
+__device__ __forceinline__ void unpack_words(uint4 u, float* f) {
+  if constexpr (sizeof(T) == 4) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  } else {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ uint4 pack_words(const float* f) {
+  if constexpr (sizeof(T) == 4) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);  // RNE (reading C7)
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// y <- y + alpha x (x broadcast when x_rows == 1: row length n)
+template <typename T>
+__global__ void __launch_bounds__(kUThreads) packed_axpy_kernel(T* __restrict__ y, const T* __restrict__ x,
+                                                               float alpha, int64_t total, int n, bool bcast,
+                                                               bool vec) {
+  constexpr int E = vec16<T>::E;
+  const int64_t nvec = vec ? total / E : 0;
+  uint4* y4 = reinterpret_cast<uint4*>(y);
+  const uint4* x4 = reinterpret_cast<const uint4*>(x);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t xv = bcast ? (v & ((n / E) - 1)) : v;
+    float fy[E], fx[E];
+    unpack_words<T>(__ldcs(y4 + v), fy);
+    unpack_words<T>(bcast ? __ldg(x4 + xv) : __ldcs(x4 + xv), fx);
+#pragma unroll
+    for (int i = 0; i < E; ++i) fy[i] = fmaf(alpha, fx[i], fy[i]);
+    __stcs(y4 + v, pack_words<T>(fy));
+  }
+  for (int64_t e = nvec * E + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t xe = bcast ? (e & (n - 1)) : e;
+    y[e] = (T)fmaf(alpha, (float)x[xe], (float)y[e]);
+  }
+}
+
+// element pair (v0, v1) store / load of T
+template <typename T>
+__device__ __forceinline__ void st_pair(T* p, T v0, T v1) {
+  if constexpr (sizeof(T) == 4) {
+    __stcs(reinterpret_cast<float2*>(p), make_float2(v0, v1));
+  } else {
+    __nv_bfloat162 h;
+    h.x = v0;
+    h.y = v1;
+    __stcs(reinterpret_cast<unsigned int*>(p), *reinterpret_cast<unsigned int*>(&h));
+  }
+}
+template <typename T>
+__device__ __forceinline__ void ld_pair(const T* p, T& v0, T& v1) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 f = __ldcs(reinterpret_cast<const float2*>(p));
+    v0 = f.x;
+    v1 = f.y;
+  } else {
+    const unsigned int u = __ldcs(reinterpret_cast<const unsigned int*>(p));
+    const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&u);
+    v0 = h.x;
+    v1 = h.y;
+  }
+}
+
+// packed rows [batch][n] -> interleaved bins [batch][n + 2]: one thread per bin k = 0 .. n/2
+template <typename T>
+__global__ void __launch_bounds__(kUThreads) decode_kernel(const T* __restrict__ p, T* __restrict__ c, int64_t batch,
+                                                          int n, int rows_per_cta) {
+  const int nb = n / 2 + 1;
+  const T zero = T(0.0f);
+  for (int64_t r0 = (int64_t)blockIdx.x * rows_per_cta; r0 < batch; r0 += (int64_t)gridDim.x * rows_per_cta) {
+    const int rows = (int)(batch - r0 < rows_per_cta ? batch - r0 : rows_per_cta);
+    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+      const int rr = e / nb, k = e - rr * nb;
+      const T* pr = p + (r0 + rr) * (int64_t)n;
+      const T re = pr[k];
+      const T im = (k == 0 || k == n / 2) ? zero : pr[n - k];
+      st_pair<T>(c + (r0 + rr) * (int64_t)(n + 2) + 2 * k, re, im);
+    }
+  }
+}
+
+// interleaved bins [batch][n + 2] -> packed rows [batch][n]
+template <typename T>
+__global__ void __launch_bounds__(kUThreads) encode_kernel(const T* __restrict__ c, T* __restrict__ p, int64_t batch,
+                                                          int n, int rows_per_cta) {
+  const int nb = n / 2 + 1;
+  for (int64_t r0 = (int64_t)blockIdx.x * rows_per_cta; r0 < batch; r0 += (int64_t)gridDim.x * rows_per_cta) {
+    const int rows = (int)(batch - r0 < rows_per_cta ? batch - r0 : rows_per_cta);
+    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
+      const int rr = e / nb, k = e - rr * nb;
+      T re, im;
+      ld_pair<T>(c + (r0 + rr) * (int64_t)(n + 2) + 2 * k, re, im);
+      T* pr = p + (r0 + rr) * (int64_t)n;
+      pr[k] = re;
+      if (k != 0 && k != n / 2) pr[n - k] = im;
+    }
+  }
+}
+
+int grid_of(int64_t work_items, int sms) {
+  const int64_t blocks = (work_items + kUThreads - 1) / kUThreads;
+  const int64_t cap = (int64_t)sms * 8;
+  return (int)(blocks < 1 ? 1 : (blocks < cap ? blocks : cap));
+}
+
+}  // namespace
+
+template <typename T>
+void launch_packed_conj(T* a, int64_t batch, int n, int logn, int sms, cudaStream_t st) {
+  const int64_t total = batch * (int64_t)n;
+  packed_conj_kernel<T><<<grid_of(total / vec16<T>::E + 1, sms), kUThreads, 0, st>>>(a, total, n, logn);
+}
+template <typename T>
+void launch_packed_axpy(T* y, const T* x, float alpha, int64_t batch, int n, bool bcast, int sms, cudaStream_t st) {
+  const int64_t total = batch * (int64_t)n;
+  // broadcast needs whole 16-byte vectors per row: n >= E (else the scalar tail loop does it all)
+  const bool vec = !bcast || n >= vec16<T>::E;  // tiny broadcast rows: scalar loop only
+  packed_axpy_kernel<T><<<grid_of(vec ? total / vec16<T>::E + 1 : total, sms), kUThreads, 0, st>>>(
+      y, x, alpha, total, n, bcast, vec);
+}
+template <typename T>
+void launch_decode(const T* p, T* c, int64_t batch, int n, int sms, cudaStream_t st) {
+  const int rows = n >= 1024 ? 1 : 1024 / n;
+  const int64_t ctas = (batch + rows - 1) / rows;
+  const int grid = (int)(ctas < (int64_t)sms * 8 ? ctas : (int64_t)sms * 8);
+  decode_kernel<T><<<grid, kUThreads, 0, st>>>(p, c, batch, n, rows);
+}
+template <typename T>
+void launch_encode(const T* c, T* p, int64_t batch, int n, int sms, cudaStream_t st) {
+  const int rows = n >= 1024 ? 1 : 1024 / n;
+  const int64_t ctas = (batch + rows - 1) / rows;
+  const int grid = (int)(ctas < (int64_t)sms * 8 ? ctas : (int64_t)sms * 8);
+  encode_kernel<T><<<grid, kUThreads, 0, st>>>(c, p, batch, n, rows);
+}
+
+#define RDFFT_UTILS_INST(T)                                                                                   \
+  template void launch_packed_conj<T>(T*, int64_t, int, int, int, cudaStream_t);                              \
+  template void launch_packed_axpy<T>(T*, const T*, float, int64_t, int, bool, int, cudaStream_t);             \
+  template void launch_decode<T>(const T*, T*, int64_t, int, int, cudaStream_t);                               \
+  template void launch_encode<T>(const T*, T*, int64_t, int, int, cudaStream_t);
+RDFFT_UTILS_INST(float)
+RDFFT_UTILS_INST(__nv_bfloat16)
+#undef RDFFT_UTILS_INST
+
+}  // namespace rdfft

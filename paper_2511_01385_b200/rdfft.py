@@ -44,8 +44,13 @@ def _lib():
         lib.bca_fwd.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_bwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_bwd_accum.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
+        lib.rdfft_decode.argtypes = [vp, vp, i64, i64, i32, vp]
+        lib.rdfft_encode.argtypes = [vp, vp, i64, i64, i32, vp]
+        lib.rdfft_packed_conj.argtypes = [vp, i64, i64, i32, vp]
+        lib.rdfft_packed_axpy.argtypes = [vp, vp, ctypes.c_float, i64, i64, i64, i32, vp]
         for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
-                  "bca_bwd_accum", "rdfft_abi_version"):
+                  "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
+                  "rdfft_abi_version"):
             getattr(lib, f).restype = i32
         lib.rdfft_status_str.argtypes = [i32]
         lib.rdfft_status_str.restype = ctypes.c_char_p
@@ -55,7 +60,8 @@ def _lib():
 
 
 EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
-           "bca_bwd_accum", "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
+           "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
+           "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
 
 
 def _ptr(t):
@@ -162,6 +168,53 @@ def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor 
     _call("bca_bwd_accum" if accumulate else "bca_bwd", _ptr(x), _ptr(w), _ptr(g), _ptr(dx), _ptr(dw),
           x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
     return dx, dw
+
+
+def rdfft_decode(p: torch.Tensor, c: torch.Tensor | None = None) -> torch.Tensor:
+    """Packed rows [..., n] -> interleaved bins [..., n + 2] (the torch.fft.rfft layout as reals;
+    `.view(torch.complex64)` of an fp32 result is the complex spectrum).  Out of place."""
+    _check(p, "p")
+    n = p.shape[-1]
+    if c is None:
+        c = torch.empty(p.shape[:-1] + (n + 2,), dtype=p.dtype, device=p.device)
+    _check(c, "c")
+    if c.dtype != p.dtype or c.shape[-1] != n + 2:
+        raise ValueError("c must be [..., n + 2] of p's dtype")
+    _call("rdfft_decode", _ptr(p), _ptr(c), p.numel() // n, n, _dtype(p), _stream(p))
+    return c
+
+
+def rdfft_encode(c: torch.Tensor, p: torch.Tensor | None = None) -> torch.Tensor:
+    """Interleaved bins [..., n + 2] -> packed rows [..., n].  Out of place."""
+    _check(c, "c")
+    n = c.shape[-1] - 2
+    if p is None:
+        p = torch.empty(c.shape[:-1] + (n,), dtype=c.dtype, device=c.device)
+    _check(p, "p")
+    if p.dtype != c.dtype or p.shape[-1] != n:
+        raise ValueError("p must be [..., n] of c's dtype")
+    _call("rdfft_encode", _ptr(c), _ptr(p), c.numel() // (n + 2), n, _dtype(c), _stream(c))
+    return p
+
+
+def rdfft_packed_conj(a: torch.Tensor) -> torch.Tensor:
+    """In place a <- conj(a) per bin (packed spectra rows).  Returns a."""
+    _check(a, "a")
+    n = a.shape[-1]
+    _call("rdfft_packed_conj", _ptr(a), a.numel() // n, n, _dtype(a), _stream(a))
+    return a
+
+
+def rdfft_packed_axpy(y: torch.Tensor, x: torch.Tensor, alpha: float) -> torch.Tensor:
+    """In place y <- y + alpha x (x: one row, broadcast, or as many rows as y).  Returns y."""
+    _check(y, "y")
+    _check(x, "x")
+    if x.dtype != y.dtype or x.shape[-1] != y.shape[-1]:
+        raise ValueError("x and y must share dtype and last dimension")
+    n = y.shape[-1]
+    _call("rdfft_packed_axpy", _ptr(y), _ptr(x), float(alpha), y.numel() // n, n, x.numel() // n, _dtype(y),
+          _stream(y))
+    return y
 
 
 def launch_count() -> int:

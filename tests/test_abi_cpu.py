@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lib):
     from paper_2511_01385_b200 import rdfft
 
     assert set(rdfft.EXPORTS) == set(declared_functions())
-    assert lib.rdfft_abi_version() == 101
+    assert lib.rdfft_abi_version() == 102
 
 
 def test_status_strings(lib):
@@ -70,6 +70,25 @@ def test_packed_validation(lib):
         assert fn(FAKE, ctypes.c_void_p(0x10010), 4, 8, 1, 0, None) == 6  # b inside a
         assert fn(FAKE, FAKE2, 4, 6, 1, 0, None) == 1
         assert fn(FAKE, FAKE2, 0, 8, 1, 0, None) == 0
+
+
+def test_utility_validation(lib):
+    far = ctypes.c_void_p(0x40000000)
+    for fn in (lib.rdfft_decode, lib.rdfft_encode):
+        assert fn(FAKE, far, 4, 12, 0, None) == 1              # E_SIZE
+        assert fn(FAKE, far, 4, 8, 9, None) == 4               # E_DTYPE
+        assert fn(FAKE, None, 4, 8, 0, None) == 2              # E_NULL
+        assert fn(FAKE, MIS, 4, 8, 0, None) == 3               # E_ALIGN
+        assert fn(FAKE, ctypes.c_void_p(0x10020), 4, 8, 0, None) == 6  # overlap (out of place only)
+        assert fn(None, None, 0, 8, 0, None) == 0
+    assert lib.rdfft_packed_conj(FAKE, 4, 6, 0, None) == 1
+    assert lib.rdfft_packed_conj(MIS, 4, 8, 0, None) == 3
+    assert lib.rdfft_packed_conj(None, 0, 8, 0, None) == 0
+    axpy = lib.rdfft_packed_axpy
+    assert axpy(FAKE, far, ctypes.c_float(1.0), 4, 8, 2, 0, None) == 5       # x_batch not in {1, batch}
+    assert axpy(FAKE, ctypes.c_void_p(0x10010), ctypes.c_float(1.0), 4, 8, 1, 0, None) == 6
+    assert axpy(FAKE, None, ctypes.c_float(1.0), 4, 8, 1, 0, None) == 2
+    assert axpy(FAKE, far, ctypes.c_float(1.0), 0, 8, 1, 0, None) == 0
 
 
 def test_bca_validation(lib):

@@ -196,6 +196,55 @@ def test_packed_mul_spec_examples(cuda_device):
     assert x.cpu().tolist() == [[1.0, 2.0, 3.0, 4.0]]
 
 
+# ------------------------------------------------ packed-spectrum utilities
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64, 1024, 4096])
+def test_decode_encode_bit_exact(n, dtype):
+    """decode / encode are permutations (plus the two explicit zeros): bit-exact vs the oracle."""
+    b = max(3, (1 << 14) // n) + 3
+    p = synth.randn((b, n), seed=200 + n, dtype=dtype).cuda()
+    c = R.rdfft_decode(p)
+    torch.cuda.synchronize()
+    assert np.array_equal(f64(c), o.decode(f64(p)))
+    p2 = R.rdfft_encode(c)
+    torch.cuda.synchronize()
+    assert torch.equal(p2, p)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64, 1024, 4096])
+def test_packed_conj_bit_exact(n, dtype):
+    b = max(3, (1 << 14) // n) + 3
+    p = synth.randn((b, n), seed=300 + n, dtype=dtype).cuda()
+    ref = o.packed_conj(f64(p))
+    R.rdfft_packed_conj(p)
+    torch.cuda.synchronize()
+    assert np.array_equal(f64(p), ref)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [2, 4, 8, 64, 1024])
+@pytest.mark.parametrize("bcast", [False, True])
+def test_packed_axpy_matches_oracle(n, dtype, bcast):
+    b = max(3, (1 << 14) // n) + 3
+    y = synth.randn((b, n), seed=400 + n, dtype=dtype).cuda()
+    x = synth.randn((1 if bcast else b, n), seed=500 + n, dtype=dtype).cuda()
+    ref = o.packed_axpy(f64(y), f64(x), -0.5)
+    R.rdfft_packed_axpy(y, x, -0.5)
+    torch.cuda.synchronize()
+    # one fp32 FMA (+ one bf16 rounding): elementwise relative error bound
+    tol = 1e-6 if dtype == "f32" else 8e-3
+    assert np.all(np.abs(f64(y) - ref) <= tol * (np.abs(ref) + 1e-30) + 1e-30)
+
+
+def test_decode_matches_torch_rfft(cuda_device):
+    """decode(rdfft_fwd(x)) viewed as complex is torch.fft.rfft(x) (fp32)."""
+    x = synth.randn((64, 512), seed=9).cuda()
+    ref = torch.fft.rfft(x)
+    c = R.rdfft_decode(R.rdfft_fwd(x.clone()))
+    assert torch.allclose(c.view(torch.complex64), ref, atol=1e-3, rtol=1e-5)
+
+
 # ------------------------------------------------------------------ BCA layer
 # fused fast paths: square q <= 4 with p in {256, 512, 1024}; the rest exercises the generic kernels
 BCA_SHAPES = [(1, 1, 2), (1, 1, 4), (2, 3, 8), (4, 2, 16), (3, 3, 64), (1, 1, 256), (3, 3, 256), (4, 4, 256),

@@ -317,3 +317,39 @@ def test_bca_bwd_zero_grad():
     x = rng(13).standard_normal((5, 12))
     dx, dw = o.bca_bwd(x, w, np.zeros((5, 8)))
     assert not dx.any() and not dw.any()
+
+
+# ------------------------------------------------ packed-spectrum utilities
+@pytest.mark.parametrize("n", [2, 4, 8, 64, 1024])
+def test_decode_is_numpy_rfft_layout(n):
+    """decode(rdfft_fwd(x)) is numpy's rfft (FFTW) bins, interleaved; encode inverts it exactly."""
+    x = rng(40 + n).standard_normal((3, n))
+    c = o.decode(o.rdfft_fwd(x))
+    ref = np.fft.rfft(x)
+    np.testing.assert_allclose(c[..., 0::2], ref.real, atol=1e-9 * n)
+    np.testing.assert_allclose(c[..., 1::2], ref.imag, atol=1e-9 * n)
+    assert np.all(c[..., 1] == 0) and np.all(c[..., n + 1] == 0)  # Im y_0 = Im y_{n/2} = 0 exactly
+    p = o.rdfft_fwd(x)
+    assert np.array_equal(o.encode(o.decode(p)), p)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 64, 1024])
+def test_packed_conj_is_time_reversal(n):
+    """conj(DFT(x)) = DFT(x[(-t) mod n]) for real x (Thm 1): conj in the packed domain equals the
+    forward transform of the time-reversed signal; conj is an involution."""
+    x = rng(50 + n).standard_normal((3, n))
+    rev = x[:, (-np.arange(n)) % n]
+    np.testing.assert_allclose(o.packed_conj(o.rdfft_fwd(x)), o.rdfft_fwd(rev), atol=1e-9 * n)
+    p = o.rdfft_fwd(x)
+    assert np.array_equal(o.packed_conj(o.packed_conj(p)), p)
+
+
+@pytest.mark.parametrize("n", [2, 8, 256])
+def test_packed_axpy_is_linear_combination(n):
+    """axpy(fwd(x), fwd(z), a) = fwd(x + a z) (linearity of Eq. 1); broadcasting of one row."""
+    x, z = rng(60 + n).standard_normal((2, 4, n))
+    a = -0.37
+    np.testing.assert_allclose(o.packed_axpy(o.rdfft_fwd(x), o.rdfft_fwd(z), a), o.rdfft_fwd(x + a * z),
+                               atol=1e-9 * n)
+    np.testing.assert_allclose(o.packed_axpy(o.rdfft_fwd(x), o.rdfft_fwd(z[0]), a), o.rdfft_fwd(x + a * z[0]),
+                               atol=1e-9 * n)
