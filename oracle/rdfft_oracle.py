@@ -61,17 +61,36 @@ def _check_n(n: int) -> None:
 
 
 @functools.lru_cache(maxsize=16)
-def _dft_matrix(n: int, nbins: int) -> np.ndarray:
-    """E[t, k] = exp(-i 2 pi k t / n) for t < n, k < nbins  (Eq. 1).
+def _roots(n: int) -> np.ndarray:
+    """r[j] = exp(-i 2 pi j / n), j < n: the n-th roots of unity of Eq. 1."""
+    ang = 2.0 * np.pi * np.arange(n, dtype=np.float64) / n
+    return np.cos(ang) - 1j * np.sin(ang)
 
-    The exponent is reduced exactly in integers, (k*t) mod n, before the
-    angle is formed, so every entry is a correctly rounded root of unity.
+
+_CHUNK = 1 << 22  # matrix entries formed at a time (bounds memory for the large sizes of N2)
+
+
+def _dft_matrix(n: int, k0: int, k1: int) -> np.ndarray:
+    """E[t, k] = exp(-i 2 pi k t / n) for t < n, k0 <= k < k1  (Eq. 1).
+
+    The exponent is reduced exactly in integers, (k*t) mod n, before the root is
+    looked up, so every entry is a correctly rounded root of unity.
     """
     t = np.arange(n, dtype=np.int64)[:, None]
-    k = np.arange(nbins, dtype=np.int64)[None, :]
-    j = (k * t) % n
-    ang = 2.0 * np.pi * j.astype(np.float64) / n
-    return np.cos(ang) - 1j * np.sin(ang)
+    k = np.arange(k0, k1, dtype=np.int64)[None, :]
+    return _roots(n)[(k * t) % n]
+
+
+def _dft_cols(x: np.ndarray, n: int, nbins: int, conj: bool = False) -> np.ndarray:
+    """x @ E[:, :nbins] (or conj(E)), formed a block of output columns at a time: every output
+    element is still the full sum over t of Eq. 1; only the columns are produced in groups."""
+    out = np.empty(x.shape[:-1] + (nbins,), dtype=np.complex128)
+    step = max(1, _CHUNK // n)
+    for k0 in range(0, nbins, step):
+        k1 = min(nbins, k0 + step)
+        E = _dft_matrix(n, k0, k1)
+        out[..., k0:k1] = x @ (np.conj(E) if conj else E)
+    return out
 
 
 def dft_full(x: np.ndarray) -> np.ndarray:
@@ -81,7 +100,7 @@ def dft_full(x: np.ndarray) -> np.ndarray:
     """
     x = np.asarray(x, dtype=np.float64)
     n = x.shape[-1]
-    return x @ _dft_matrix(n, n)
+    return _dft_cols(x, n, n)
 
 
 def dft(x: np.ndarray) -> np.ndarray:
@@ -89,7 +108,7 @@ def dft(x: np.ndarray) -> np.ndarray:
     x = np.asarray(x, dtype=np.float64)
     n = x.shape[-1]
     _check_n(n)
-    return x @ _dft_matrix(n, n // 2 + 1)
+    return _dft_cols(x, n, n // 2 + 1)
 
 
 def pack(Y: np.ndarray, n: int | None = None) -> np.ndarray:
@@ -142,7 +161,7 @@ def idft(Y: np.ndarray) -> np.ndarray:
     """Inverse DFT, x_t = (1/n) sum_k y_k e^{+i 2 pi k t / n}  (Eq. 1). Complex out."""
     Y = np.asarray(Y, dtype=np.complex128)
     n = Y.shape[-1]
-    return (Y @ np.conj(_dft_matrix(n, n))) / n
+    return _dft_cols(Y, n, n, conj=True) / n
 
 
 def rdfft_inv(p: np.ndarray) -> np.ndarray:

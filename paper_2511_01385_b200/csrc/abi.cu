@@ -24,7 +24,11 @@ int ilog2(int64_t n) {
   while ((int64_t(1) << l) < n) ++l;
   return l;
 }
+// BCA blocks: 2 <= p <= 4096 (reading C9); transforms, packed products and the utilities also
+// take the large sizes of SURVEY §8(f) N2, n <= 32768 (planl.cuh).
+constexpr int64_t kMaxTransformN = 32768;
 bool pow2_in_range(int64_t n) { return n >= 2 && n <= kMaxN && (n & (n - 1)) == 0; }
+bool pow2_transform(int64_t n) { return n >= 2 && n <= kMaxTransformN && (n & (n - 1)) == 0; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 bool overlap(const void* a, size_t na, const void* b, size_t nb) {
   const char* pa = static_cast<const char*>(a);
@@ -65,7 +69,7 @@ int launch_transform(T* x, int64_t batch, int n, bool inverse, cudaStream_t st) 
 
 int transform(void* x, int64_t batch, int64_t n, int dtype, void* stream, bool inverse) {
   if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return RDFFT_E_DTYPE;
-  if (!pow2_in_range(n)) return RDFFT_E_SIZE;
+  if (!pow2_transform(n)) return RDFFT_E_SIZE;
   if (batch < 0) return RDFFT_E_SHAPE;
   if (batch == 0) return RDFFT_OK;
   if (!x) return RDFFT_E_NULL;
@@ -77,7 +81,7 @@ int transform(void* x, int64_t batch, int64_t n, int dtype, void* stream, bool i
 
 int packed(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, int dtype, void* stream, bool conj) {
   if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return RDFFT_E_DTYPE;
-  if (!pow2_in_range(n)) return RDFFT_E_SIZE;
+  if (!pow2_transform(n)) return RDFFT_E_SIZE;
   if (batch < 0 || b_batch < 0) return RDFFT_E_SHAPE;
   if (batch == 0) return RDFFT_OK;
   if (b_batch != 1 && b_batch != batch) return RDFFT_E_SHAPE;
@@ -87,6 +91,15 @@ int packed(void* a, const void* b, int64_t batch, int64_t n, int64_t b_batch, in
   if (overlap(a, batch * n * s, b, b_batch * n * s) && !(a == b && b_batch == batch)) return RDFFT_E_ALIAS;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logn = ilog2(n);
+  if (n > kMaxN) {  // rows longer than the tiled kernels' tiles
+    if (dtype == RDFFT_F32)
+      launch_packed_mul_large<float>(static_cast<float*>(a), static_cast<const float*>(b), batch, (int)n,
+                                     b_batch == 1 && batch > 1, conj, num_sms(), st);
+    else
+      launch_packed_mul_large<__nv_bfloat16>(static_cast<__nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(b),
+                                             batch, (int)n, b_batch == 1 && batch > 1, conj, num_sms(), st);
+    return launched();
+  }
   if (n >= 16 && aligned16(a) && aligned16(b)) {
     const int rows = (kPm2TileBytes / (int)s) >> logn;
     const int64_t tiles = (batch + rows - 1) / rows;
@@ -169,7 +182,7 @@ int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, in
 // shared validation of the packed-spectrum utilities: 1 = proceed, 0 = no-op, < 0 = -status
 int util_check(const void* a, const void* b, int64_t batch, int64_t n, int dtype) {
   if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return -RDFFT_E_DTYPE;
-  if (!pow2_in_range(n)) return -RDFFT_E_SIZE;
+  if (!pow2_transform(n)) return -RDFFT_E_SIZE;
   if (batch < 0) return -RDFFT_E_SHAPE;
   if (batch == 0) return 0;
   if (!a || !b) return -RDFFT_E_NULL;
@@ -389,7 +402,7 @@ int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* 
 const char* rdfft_status_str(int status) {
   switch (status) {
     case RDFFT_OK: return "ok";
-    case RDFFT_E_SIZE: return "n (or p) is not a power of two in [2, 4096]";
+    case RDFFT_E_SIZE: return "n is not a power of two in [2, 32768] (BCA block p: [2, 4096])";
     case RDFFT_E_NULL: return "null pointer";
     case RDFFT_E_ALIGN: return "pointer not 16-byte aligned";
     case RDFFT_E_DTYPE: return "unsupported dtype";
@@ -402,6 +415,6 @@ const char* rdfft_status_str(int status) {
 
 uint64_t rdfft_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int rdfft_abi_version(void) { return 102; }
+int rdfft_abi_version(void) { return 103; }
 
 }  // extern "C"

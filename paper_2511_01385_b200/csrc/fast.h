@@ -24,4 +24,6 @@ template <typename T>
 void launch_decode(const T* p, T* c, int64_t batch, int n, int sms, cudaStream_t st);
 template <typename T>
 void launch_encode(const T* c, T* p, int64_t batch, int n, int sms, cudaStream_t st);
+template <typename T>
+void launch_packed_mul_large(T* a, const T* b, int64_t batch, int n, bool bcast, bool conj, int sms, cudaStream_t st);
 }  // namespace rdfft

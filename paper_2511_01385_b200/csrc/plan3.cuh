@@ -13,6 +13,7 @@
 #include "plan2.cuh"
 #include "plan2o.cuh"
 #include "small.cuh"
+#include "planl.cuh"
 
 namespace rdfft {
 
@@ -526,6 +527,9 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
     case 1024: return launch_p2<T, 1024, 32, 8>(x, batch, inverse, sms, st);
     case 2048: return launch_plan3<Plan3<T, 2048, 4, 1>>(x, batch, inverse, sms, st);
     case 4096: return launch_plan3<Plan3<T, 4096, 2, 1>>(x, batch, inverse, sms, st);
+    case 8192: return launch_planl<PlanL<T, 8192>>(x, batch, inverse, sms, st);
+    case 16384: return launch_planl<PlanL<T, 16384>>(x, batch, inverse, sms, st);
+    case 32768: return launch_planl<PlanL<T, 32768>>(x, batch, inverse, sms, st);
     default: return false;
   }
 }

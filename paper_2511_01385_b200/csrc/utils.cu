@@ -184,6 +184,29 @@ __global__ void __launch_bounds__(kUThreads) encode_kernel(const T* __restrict__
   }
 }
 
+// a <- a (.) [conj] b per bin for rows longer than the tiled kernel's 16 KB tiles (n > 4096):
+// one thread per bin k = 0 .. n/2 of a row, (slot k, slot n - k) pairs.
+template <typename T, bool kConj>
+__global__ void __launch_bounds__(kUThreads) packed_mul_large_kernel(T* __restrict__ a, const T* __restrict__ b,
+                                                                    int64_t batch, int n, bool bcast) {
+  const int nb = n / 2 + 1;
+  const int64_t total = batch * nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / nb;
+    const int k = (int)(e - r * nb);
+    T* ar = a + r * n;
+    const T* br = b + (bcast ? 0 : r * n);
+    if (k == 0 || k == n / 2) {  // real bins
+      ar[k] = (T)((float)ar[k] * (float)br[k]);
+    } else {
+      const float xr = (float)ar[k], xi = (float)ar[n - k];
+      const float yr = (float)br[k], yi = kConj ? -(float)br[n - k] : (float)br[n - k];
+      ar[k] = (T)fmaf(xr, yr, -xi * yi);
+      ar[n - k] = (T)fmaf(xr, yi, xi * yr);
+    }
+  }
+}
+
 int grid_of(int64_t work_items, int sms) {
   const int64_t blocks = (work_items + kUThreads - 1) / kUThreads;
   const int64_t cap = (int64_t)sms * 8;
@@ -220,11 +243,21 @@ void launch_encode(const T* c, T* p, int64_t batch, int n, int sms, cudaStream_t
   encode_kernel<T><<<grid, kUThreads, 0, st>>>(c, p, batch, n, rows);
 }
 
+template <typename T>
+void launch_packed_mul_large(T* a, const T* b, int64_t batch, int n, bool bcast, bool conj, int sms, cudaStream_t st) {
+  const int grid = grid_of(batch * (n / 2 + 1), sms);
+  if (conj)
+    packed_mul_large_kernel<T, true><<<grid, kUThreads, 0, st>>>(a, b, batch, n, bcast);
+  else
+    packed_mul_large_kernel<T, false><<<grid, kUThreads, 0, st>>>(a, b, batch, n, bcast);
+}
+
 #define RDFFT_UTILS_INST(T)                                                                                   \
   template void launch_packed_conj<T>(T*, int64_t, int, int, int, cudaStream_t);                              \
   template void launch_packed_axpy<T>(T*, const T*, float, int64_t, int, bool, int, cudaStream_t);             \
   template void launch_decode<T>(const T*, T*, int64_t, int, int, cudaStream_t);                               \
-  template void launch_encode<T>(const T*, T*, int64_t, int, int, cudaStream_t);
+  template void launch_encode<T>(const T*, T*, int64_t, int, int, cudaStream_t);                               \
+  template void launch_packed_mul_large<T>(T*, const T*, int64_t, int, bool, bool, int, cudaStream_t);
 RDFFT_UTILS_INST(float)
 RDFFT_UTILS_INST(__nv_bfloat16)
 #undef RDFFT_UTILS_INST

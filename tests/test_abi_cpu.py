@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lib):
     from paper_2511_01385_b200 import rdfft
 
     assert set(rdfft.EXPORTS) == set(declared_functions())
-    assert lib.rdfft_abi_version() == 102
+    assert lib.rdfft_abi_version() == 103
 
 
 def test_status_strings(lib):
@@ -55,7 +55,7 @@ def test_transform_validation(lib):
     for fn in (lib.rdfft_fwd, lib.rdfft_inv):
         assert fn(FAKE, 4, 3, 0, None) == 1        # E_SIZE: not a power of two
         assert fn(FAKE, 4, 1, 0, None) == 1        # E_SIZE: n = 1
-        assert fn(FAKE, 4, 8192, 0, None) == 1     # E_SIZE: above 4096
+        assert fn(FAKE, 4, 65536, 0, None) == 1    # E_SIZE: above 32768
         assert fn(FAKE, 4, 8, 7, None) == 4        # E_DTYPE
         assert fn(FAKE, -1, 8, 0, None) == 5       # E_SHAPE
         assert fn(None, 4, 8, 0, None) == 2        # E_NULL
@@ -94,6 +94,7 @@ def test_utility_validation(lib):
 def test_bca_validation(lib):
     y = ctypes.c_void_p(0x40000000)
     assert lib.bca_fwd(FAKE, FAKE2, y, 4, 768, 768, 100, 1, None) == 1      # p not pow2
+    assert lib.bca_fwd(FAKE, FAKE2, y, 4, 8192, 8192, 8192, 1, None) == 1   # p above 4096
     assert lib.bca_fwd(FAKE, FAKE2, y, 4, 770, 768, 256, 1, None) == 5      # d_in % p
     assert lib.bca_fwd(FAKE, FAKE2, y, 4, 768, 768, 256, 3, None) == 4      # dtype
     assert lib.bca_fwd(FAKE, FAKE2, None, 4, 768, 768, 256, 1, None) == 2   # y null

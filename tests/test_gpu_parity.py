@@ -196,6 +196,59 @@ def test_packed_mul_spec_examples(cuda_device):
     assert x.cpu().tolist() == [[1.0, 2.0, 3.0, 4.0]]
 
 
+# ------------------------------------------------ large n (planl.cuh)
+NL = [8192, 16384, 32768]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", NL)
+def test_large_n_forward_inverse(n, dtype):
+    """One vector per CTA: a batch above the grid (persistent loop) with sampled rows against the
+    oracle (forward and inverse), the round trip on every row, and exact placement probes."""
+    b = 2 * 148 + 7
+    x = synth.randn((b, n), seed=700 + n, dtype=dtype).cuda()
+    x[0].zero_()
+    x[0, 0] = 1  # impulse -> exactly ones in slots 0 .. n/2, zeros elsewhere (P2)
+    x0 = x.clone()
+    rows = [1, b - 1] if n < 32768 else [b - 1]
+    xin = f64(x[rows])
+    R.rdfft_fwd(x)
+    torch.cuda.synchronize()
+    imp = np.zeros(n)
+    imp[: n // 2 + 1] = 1
+    assert np.array_equal(f64(x[0]), imp)
+    assert rel_l2_rows(f64(x[rows]), o.rdfft_fwd(xin)) <= TOL[dtype]
+    pin = f64(x[rows[:1]])
+    R.rdfft_inv(x)
+    torch.cuda.synchronize()
+    assert rel_l2_rows(f64(x[rows[:1]]), o.rdfft_inv(pin)) <= TOL[dtype]
+    err = (x.float() - x0.float()).norm(dim=1) / x0.float().norm(dim=1)
+    assert float(err.max()) <= (2e-5 if dtype == "f32" else 2e-2)
+    # inverse probes: e_0 -> 1/n exactly, e_{n/2} -> (-1)^t / n exactly
+    e = torch.zeros((2, n), dtype=x.dtype, device="cuda")
+    e[0, 0] = 1
+    e[1, n // 2] = 1
+    R.rdfft_inv(e)
+    torch.cuda.synchronize()
+    t = np.arange(n)
+    assert np.array_equal(f64(e[0]), np.full(n, 1.0 / n))
+    assert np.array_equal(f64(e[1]), (-1.0) ** t / n)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("conj", [False, True])
+def test_large_n_packed_mul(dtype, conj):
+    n, b = 8192, 7
+    a = synth.randn((b, n), seed=61, dtype=dtype).cuda()
+    for bb in (1, b):
+        w = synth.randn((bb, n), seed=62 + bb, dtype=dtype).cuda()
+        ref = (o.packed_conjmul if conj else o.packed_mul)(f64(a), f64(w))
+        out = a.clone()
+        (R.rdfft_packed_conjmul if conj else R.rdfft_packed_mul)(out, w)
+        torch.cuda.synchronize()
+        assert rel_l2_rows(f64(out), ref) <= TOL[dtype]
+
+
 # ------------------------------------------------ packed-spectrum utilities (SURVEY §8(f) N3)
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("n", [2, 4, 8, 16, 64, 1024, 4096])
