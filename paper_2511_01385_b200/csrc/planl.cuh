@@ -31,7 +31,13 @@ struct PlanL {
   static constexpr int R = 32, LR = 5, S = N / R, LS = LN - LR;
   static constexpr int M2 = 32, W2 = 1024, NW2 = N / W2;
   static constexpr int M3 = N / W2, LM3 = ilog2c<M3>(), K3 = W2 / 2;
-  static constexpr int NT = 512;  // 16 warps: 4 per SM quadrant keeps the 128-register budget
+  // threads: one per pass-1 subsequence pair and per pass-2 set (S/2 = 16 NW2), <= 16 warps (4 per
+  // SM quadrant keeps the 128-register budget); pass 3 loops over K3 / NT sets per thread.  Small n
+  // thus runs several CTAs per SM (n = 8192: 128 threads, 4 CTAs; 16384: 256 threads, 2 CTAs).
+  static constexpr int NT = S / 2 < 512 ? S / 2 : 512;
+  static constexpr int K3PT = K3 / NT;
+  static constexpr int MINB = 512 / NT;  // CTAs per SM the 128-register budget allows
+  static_assert(S / 2 == NW2 * 16 || NT == 512, "pass-2 sets per thread");
   static constexpr int TW2N = 32 * 16, TW3N = (M3 / 4) * K3;
   static constexpr size_t TW2_OFF = (size_t)N * 4;
   static constexpr size_t TW3_OFF = TW2_OFF + (size_t)TW2N * 8;
@@ -174,7 +180,7 @@ struct gio4<__nv_bfloat16> {
 };
 
 template <typename P, bool kInv>
-__global__ void __launch_bounds__(P::NT, 1) rdfftl_kernel(typename P::elem* __restrict__ x, int64_t batch) {
+__global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem* __restrict__ x, int64_t batch) {
   using T = typename P::elem;
   constexpr int N = P::N, NT = P::NT, R = P::R, S = P::S, K3 = P::K3, M3 = P::M3;
   extern __shared__ float4 smem4[];
@@ -196,20 +202,29 @@ __global__ void __launch_bounds__(P::NT, 1) rdfftl_kernel(typename P::elem* __re
     sincospif(2.0f * (float)(4 * k * a) / (float)N, &s, &c);
     TW3[e] = kInv ? make_float2(c * (1.0f / N), s * (1.0f / N)) : make_float2(c, -s);
   }
-  // pass-3 lane: k3 = 1 .. 511, and lane 0 takes the zero-imaginary set k3 = 512 plus the DC set
-  // (two real-input sets ~ one complex set of work)
-  const int k3 = tid == 0 ? K3 : tid;
-  LTw3<K3> tw3;
-  tw3.h = TW3 + (k3 - 1);
-  {
+  // pass-3 sets k3 = tid + NT i (i < K3PT); k3 = 0 stands for the zero-imaginary set k3 = 512
+  // plus the DC set (two real-input sets ~ one complex set of work)
+  auto tw3_for = [&](int k3) {
+    LTw3<K3> t;
+    t.h = TW3 + (k3 - 1);
     float s, c;
     sincospif(2.0f * (float)k3 / (float)N, &s, &c);
-    tw3.w1 = make_float2(c, sg * s);
+    t.w1 = make_float2(c, sg * s);
     sincospif(4.0f * (float)k3 / (float)N, &s, &c);
-    tw3.w2 = make_float2(c, sg * s);
+    t.w2 = make_float2(c, sg * s);
     sincospif(6.0f * (float)k3 / (float)N, &s, &c);
-    tw3.w3 = make_float2(c, sg * s);
-  }
+    t.w3 = make_float2(c, sg * s);
+    return t;
+  };
+  auto pass3 = [&](auto inv) {
+    constexpr bool kI = decltype(inv)::value;
+#pragma unroll 1
+    for (int i = 0; i < P::K3PT; ++i) {
+      const int kk = tid + NT * i, k3 = kk == 0 ? K3 : kk;
+      pl_set<P, M3, kI>(H, 0, 1024, k3, tw3_for(k3));
+      if (kk == 0) pl_dc<P, M3, kI>(H, 0, 1024, kI ? 1.0f / N : 1.0f);
+    }
+  };
   // pass-2 lane: window ww, k2 = 1 .. 15; lane 0 of each window: k2 = 16 (zero imaginary) + DC
   const int ww = tid / 16, k2 = tid % 16 == 0 ? 16 : tid % 16;
   const bool act2 = tid < P::NW2 * 16;
@@ -239,8 +254,7 @@ __global__ void __launch_bounds__(P::NT, 1) rdfftl_kernel(typename P::elem* __re
       if (act2) pl_set<P, 32, false>(H, ww * 1024, 32, k2, tw2);
       if (act2 && k2 == 16) pl_dc<P, 32, false>(H, ww * 1024, 32, 1.0f);
       __syncthreads();
-      pl_set<P, M3, false>(H, 0, 1024, k3, tw3);
-      if (tid == 0) pl_dc<P, M3, false>(H, 0, 1024, 1.0f);
+      pass3(std::false_type{});
       __syncthreads();
       for (int e = tid; e < N / 4; e += NT) {
         const float4 f = *reinterpret_cast<const float4*>(H + P::phys(4 * e));
@@ -251,8 +265,7 @@ __global__ void __launch_bounds__(P::NT, 1) rdfftl_kernel(typename P::elem* __re
       for (int e = tid; e < N / 4; e += NT)
         *reinterpret_cast<float4*>(H + P::phys(4 * e)) = gio4<T>::ld(xv + 4 * e);
       __syncthreads();
-      pl_set<P, M3, true>(H, 0, 1024, k3, tw3);
-      if (tid == 0) pl_dc<P, M3, true>(H, 0, 1024, 1.0f / N);
+      pass3(std::true_type{});
       __syncthreads();
       if (act2) pl_set<P, 32, true>(H, ww * 1024, 32, k2, tw2);
       if (act2 && k2 == 16) pl_dc<P, 32, true>(H, ww * 1024, 32, 1.0f);
