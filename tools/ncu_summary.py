@@ -100,7 +100,7 @@ def main():
     if a.bench and os.path.exists(a.bench):
         b = json.loads(open(a.bench).read().strip().splitlines()[-1])
         md.append("## bench line (CUDA events, not under ncu)\n")
-        md.append(f"- value: {b['value']:.1f} {b['unit']} ({100 * b.get('frac_of_hbm_peak', 0):.1f}% of measured HBM)")
+        md.append(f"- value: {b['value']:.1f} {b['unit']} ({100 * b.get('frac_of_hbm_peak', 0):.1f}% of the bench peak)")
         md.append(f"- segments (ms per step): " + ", ".join(f"{k} {v:.3f}" for k, v in b["segments_ms"].items()))
         md.append(f"- clocks: {b.get('clocks')}\n")
     if a.launches and os.path.exists(a.launches):
