@@ -142,7 +142,8 @@ struct P2Roles {
   int v2, k;         // last pass: vector v2, set k
   float2* ha;        //   slots j R + k
   float2* hm;        //   slots (j+1) R - k
-  float2* hmz;       //   imaginary input (fwd) / output (inv): pad for k = R/2
+  float2* hmz;       //   imaginary input (fwd): the zero pad for k = R/2
+  bool kz;           //   k == R/2: the inverse discards the imaginary output (the pad stays zero)
   const float2* twf; //   forward twiddles (column k - 1)
   const float2* twi; //   inverse twiddles
   int dv;            // DC set: lane dv of the last warp (dv < 0: none)
@@ -168,7 +169,8 @@ struct P2Roles {
     k = 1 + (P::kInterleave ? (lt % 32) / VPW : lt % P::LPV);
     ha = H + P::row(v2) + k;
     hm = H + P::row(v2) + (R - k);
-    hmz = (k == R / 2) ? (H + P::row(v2) + R) : hm;
+    kz = (k == R / 2);
+    hmz = kz ? (H + P::row(v2) + R) : hm;
     twf = TWf + (k - 1) * P::TWS;
     twi = TWi + (k - 1) * P::TWS;
     dv = lt - P::DC0;
@@ -360,7 +362,9 @@ __device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv) {
       constexpr int jj = decltype(J)::value;
       constexpr int r1 = rev_bits<LM>(jj), r2 = rev_bits<LM>(jj + M / 2);
       r.ha[jj * WSTR] = make_float2(zr[r1], zr[r2]);
-      r.hmz[jj * WSTR] = make_float2(zi[r1], zi[r2]);  // k = R/2: imaginary part discarded into the pad
+      // k = R/2: the imaginary part (zero up to rounding) is dropped, so the pad keeps the exact
+      // zero the next forward pass of the same buffer reads (fused BCA kernels reuse H per tile)
+      if (!r.kz) r.hm[jj * WSTR] = make_float2(zi[r1], zi[r2]);
     });
   }
 }

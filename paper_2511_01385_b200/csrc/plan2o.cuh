@@ -65,7 +65,7 @@ __device__ __forceinline__ void p2o_last_inv(const P2Roles<P>& r, const __nv_bfl
       constexpr int jj = decltype(J)::value;
       constexpr int r1 = rev_bits<LM>(jj), r2 = rev_bits<LM>(jj + M / 2);
       r.ha[jj * P::WSTR] = make_float2(zr[r1], zr[r2]);
-      r.hmz[jj * P::WSTR] = make_float2(zi[r1], zi[r2]);
+      if (!r.kz) r.hm[jj * P::WSTR] = make_float2(zi[r1], zi[r2]);  // k = R/2: imaginary part dropped
     });
   }
 }

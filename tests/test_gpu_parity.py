@@ -451,3 +451,27 @@ def test_host_pipeline_matches_device_calls():
     R.rdfft_inv(ref)
     torch.cuda.synchronize()
     assert torch.equal(xh, ref.cpu())
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("q,p", [(4, 1024), (3, 256), (4, 256), (2, 512), (2, 64), (16, 256)])
+def test_bca_no_state_between_tiles(dtype, q, p):
+    """Every token tile is independent: a CTA that first processes tiles of huge tokens and then
+    tiles of tiny ones must give the tiny ones their own relative accuracy (no value left in
+    shared memory by one tile may reach the next)."""
+    T = 2 * 148 * 2 * 16  # every CTA / pipe runs at least two tiles
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=21, dtype=dtype)
+    scale = torch.ones(T, 1)
+    scale[: T // 2] = 1e4
+    scale[T // 2:] = 1e-4
+    x = (x.float() * scale).to(x.dtype)
+    g = (g.float() * scale).to(g.dtype)
+    xc, wc, gc = x.cuda(), w.cuda(), g.cuda()
+    y = R.bca_fwd(xc, wc)
+    dx, _ = R.bca_bwd(xc, wc, gc)
+    torch.cuda.synchronize()
+    rows = [T - 1, T - 2, T // 2, T // 2 + 7, 3 * T // 4]
+    xo, wo, go = f64(x[rows]), f64(w), f64(g[rows])
+    assert rel_l2_rows(f64(y[rows]), o.bca_fwd(xo, wo)) <= TOL[dtype]
+    dxo, _ = o.bca_bwd(xo, wo, go)
+    assert rel_l2_rows(f64(dx[rows]), dxo) <= TOL[dtype]
