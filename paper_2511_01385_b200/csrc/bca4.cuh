@@ -95,50 +95,4 @@ bool launch_bca_fwd4(const typename P::elem* x, const typename P::elem* w, typen
   return true;
 }
 
-// bf16: the 2-pipe kernel (LLaMA shape 0.190 -> 0.163 ms measured); fp32 keeps the staged
-// single-pipe kernel (its 8-byte direct loads made the 2-pipe variant slower: 0.194 -> 0.205 ms).
-// RDFFT_BCA_FWD4=0 selects the single-pipe kernel for bf16 too, for comparison.
-inline bool use_fwd4() {
-  static const bool v = [] {
-    const char* e = std::getenv("RDFFT_BCA_FWD4");
-    return !(e && *e == '0');
-  }();
-  return v;
-}
-
-#ifndef RDFFT_BCA_FWD_VT
-#define RDFFT_BCA_FWD_VT 16   // p = 1024 forward: 32 vectors (8 tokens of q = 4) per tile, 512 threads
-#endif
-#ifndef RDFFT_BCA_FWD_NSTG
-#define RDFFT_BCA_FWD_NSTG 2  // ... with pass 1 reading x straight from HBM (H + W fill shared memory)
-#endif
-// Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
-template <typename T, int Q>
-bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st) {
-  switch (p) {
-    case 256:
-      if constexpr (sizeof(T) == 2)
-        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 256, 16, 16>, Q, 2>(x, w, y, T_, sms, st);
-      return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
-    case 1024:
-      if constexpr (sizeof(T) == 2)
-        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st);
-      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
-          x, w, y, T_, sms, st);
-    default: return false;
-  }
-}
-template <typename T>
-bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
-  if (q_in != q_out) return false;
-  switch (q_in) {
-    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st);
-    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st);
-    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st);
-    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st);
-    default: return false;
-  }
-}
-
 }  // namespace rdfft

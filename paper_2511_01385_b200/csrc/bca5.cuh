@@ -1,0 +1,274 @@
+// bca5.cuh — BCA forward for the LLaMA block size (p = 1024, bf16) with the W spectra in
+// TENSOR MEMORY.  The 64 KB of fp32 W spectra (q^2 <= 16 blocks) are what limit bca_fwd4 to one
+// shared-memory copy and no input staging; here they live in TMEM (256 KB per SM, read with
+// tcgen05.ld on a datapath separate from shared memory), which frees shared memory for a TMA
+// staging buffer per pipe, so every pipe prefetches its next token tile while it computes.
+//
+// TMEM layout (128 columns, one allocation per CTA): the product thread of item u (bins u and
+// N/2 - u, see bca2.cuh) of either pipe sits in TMEM lane u % 128 (warp w may only access lanes
+// 32 (w % 4) .. + 31, and thread t of a pipe is in warp t / 32); item u's 16 bin pairs W_ij
+// (4 fp32 each) are columns 64 (u / 128) .. + 63 of that lane.
+//
+// Per tile and pipe (Eq. 4; blocks P:L184), as bca_fwd4_kernel:
+//   wait staged x tile -> X = rdFFT(x) -> issue the next tile's TMA -> Y_i = sum_j W_ij (.) X_j
+//   (W from TMEM) -> y = IrdFFT(Y) straight to HBM.  x is never written (reading C13).
+#pragma once
+
+#include "bca4.cuh"
+
+namespace rdfft {
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+               : "memory");
+}
+// Wait for this thread's outstanding tcgen05.ld; the registers are in/out operands so no use of
+// them can be scheduled above the wait.
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <typename P, int PIPES>
+struct BcaFwd5Smem {  // [stage x PIPES][H x PIPES][TWf][TWi][bars x PIPES][tmem addr]
+  static constexpr size_t H_OFF = (size_t)PIPES * P::STAGE;
+  static constexpr size_t TWF_OFF = H_OFF + (size_t)PIPES * P::HF * 8;
+  static constexpr size_t TWI_OFF = TWF_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BAR_OFF = TWI_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t TMEM_OFF = BAR_OFF + 8 * PIPES;
+  static constexpr size_t BYTES = TMEM_OFF + 16;
+};
+
+template <typename P, int Q, int PIPES>
+__global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typename P::elem* __restrict__ x,
+                                                                   const typename P::elem* __restrict__ w,
+                                                                   typename P::elem* __restrict__ y, int64_t T_) {
+  constexpr int q = Q;
+  using T = typename P::elem;
+  using L = BcaFwd5Smem<P, PIPES>;
+  constexpr int N = P::N, NT = P::NT, NI = N / 4;
+  static_assert(NT == NI && NI == 256, "one product item per thread, two items per TMEM lane");
+  static_assert(Q * Q <= P::VT && PIPES >= 2, "W prologue uses pipe 1's H region as scratch");
+  constexpr uint32_t kCols = 128;
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  const int tid = threadIdx.x;
+  const int pipe = tid / NT, lt = tid % NT;
+  float2* Hbase = reinterpret_cast<float2*>(base + L::H_OFF);
+  float2* H = Hbase + (size_t)pipe * P::HF;
+  float2* TWf = reinterpret_cast<float2*>(base + L::TWF_OFF);
+  float2* TWi = reinterpret_cast<float2*>(base + L::TWI_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF) + pipe;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::TMEM_OFF);
+  unsigned char* stg = base + (size_t)pipe * P::STAGE;
+  const int TT = P::VT / q;
+  const int64_t ntiles = (T_ + TT - 1) / TT;
+  const int64_t tok_elems = (int64_t)q * N;
+  auto tile_rows = [&](int64_t t) { return (int)((T_ - t * TT < TT ? T_ - t * TT : TT) * q); };
+  if (tid < 32) {  // warp 0 owns the TMEM allocation
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  p2_tables<P>(TWf, TWi, tid, PIPES * NT);
+  for (int pp = 0; pp < PIPES; ++pp) p2_zero_pads<P>(Hbase + (size_t)pp * P::HF, P::VT, tid, PIPES * NT);
+  if (tid == 0) {
+    for (int pp = 0; pp < PIPES; ++pp) mbar_init(bar - pipe + pp, 1);
+    fence_mbar_init();
+  }
+  const uint32_t k65536 = kTwo16;
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM address of this thread's item (lane = warp quarter base + lane in warp; 64 columns per item)
+  const int u = lt;
+  const uint32_t taddr = tmem + ((uint32_t)(32 * ((tid / 32) % 4)) << 16) + (uint32_t)(64 * (u / 128));
+  // ---- first tile of each pipe: start its TMA while W is being transformed
+  if (lt == 0) {
+    const int64_t t = (int64_t)blockIdx.x * PIPES + pipe;
+    if (t < ntiles) stage_issue_rows<P>(x + t * TT * tok_elems, tile_rows(t), stg, bar);
+  }
+  // ---- prologue: W_ij = rdFFT(w_ij) into pipe 1's H (scratch), then into TMEM by pipe 0
+  float2* Wtmp = Hbase + (size_t)(PIPES - 1) * P::HF;
+  if (pipe == 0) {
+    const P2Roles<P> rw(Wtmp, TWf, TWi, lt);
+    p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
+    named_bar(1, NT);
+    p2_last_fwd<P>(rw, q * q);
+    p2_dc_fwd<P>(rw, q * q);
+    named_bar(1, NT);
+    int oa, ob;
+    bca_item_offsets<P>(u, oa, ob);
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {  // 4 groups of 4 bin pairs = 16 columns each
+      uint32_t r[16];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int c = 4 * g4 + c4;
+        BinPair b = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        if (c < q * q) b = bins_get(Wtmp + P::row(c), oa, ob, u == 0);
+        r[4 * c4 + 0] = __float_as_uint(b.b1.x);
+        r[4 * c4 + 1] = __float_as_uint(b.b1.y);
+        r[4 * c4 + 2] = __float_as_uint(b.b2.x);
+        r[4 * c4 + 3] = __float_as_uint(b.b2.y);
+      }
+      tmem_st16(taddr + 16 * g4, r);
+    }
+    tmem_wait_st();
+  }
+  tmem_fence_before();
+  __syncthreads();  // W in TMEM; pipe 1's H free again (the forward never writes the pads)
+  tmem_fence_after();
+  const P2Roles<P> rh(H, TWf, TWi, lt);
+  const int bid = 1 + pipe;
+  int oa, ob;
+  bca_item_offsets<P>(u, oa, ob);
+  const bool special = (u == 0);
+  uint32_t phase = 0;
+  for (int64_t tile = (int64_t)blockIdx.x * PIPES + pipe; tile < ntiles; tile += (int64_t)gridDim.x * PIPES) {
+    const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
+    const int nv = ntok * q;
+    mbar_wait(bar, phase & 1);
+    ++phase;
+    p2_pass1_fwd<P>(rh, reinterpret_cast<const T*>(stg), nv, k65536);
+    named_bar(bid, NT);  // H complete; staging consumed
+    const int64_t nxt = tile + (int64_t)gridDim.x * PIPES;
+    if (lt == 0 && nxt < ntiles) stage_issue_rows<P>(x + nxt * TT * tok_elems, tile_rows(nxt), stg, bar);
+    p2_last_fwd<P>(rh, nv);
+    p2_dc_fwd<P>(rh, nv);
+    named_bar(bid, NT);
+    {  // ---- product, W_ij from TMEM
+      BinPair wv[Q][Q];
+#pragma unroll
+      for (int g4 = 0; g4 < 4; ++g4) {
+        if (4 * g4 < q * q) {
+          uint32_t r[16];
+          tmem_ld16(taddr + 16 * g4, r);
+          tmem_wait_ld(r);
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const int c = 4 * g4 + c4;
+            if (c < q * q)
+              wv[c / Q][c % Q] = {make_float2(__uint_as_float(r[4 * c4]), __uint_as_float(r[4 * c4 + 1])),
+                                  make_float2(__uint_as_float(r[4 * c4 + 2]), __uint_as_float(r[4 * c4 + 3]))};
+          }
+        }
+      }
+      for (int tt = 0; tt < ntok; ++tt) {
+        PrepB x1[Q];
+        float2 x2[Q];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          const BinPair xb = bins_get(H + P::row(tt * q + j), oa, ob, special);
+          x1[j] = prep_b<false>(xb.b1, special);
+          x2[j] = xb.b2;
+        }
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          BinPair yv = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int j = 0; j < Q; ++j) {
+            yv.b1 = pmac(wv[i][j].b1, x1[j], yv.b1);
+            yv.b2 = cfma(wv[i][j].b2, x2[j], yv.b2);
+          }
+          bins_put(H + P::row(tt * q + i), oa, ob, special, yv);
+        }
+      }
+    }
+    named_bar(bid, NT);
+    p2_last_inv<P>(rh, nv);
+    p2_dc_inv<P>(rh, nv);
+    named_bar(bid, NT);
+    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv);
+    named_bar(bid, NT);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
+}
+
+template <typename P, int Q, int PIPES>
+bool launch_bca_fwd5(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
+                     cudaStream_t st) {
+  using L = BcaFwd5Smem<P, PIPES>;
+  auto k = bca_fwd5_kernel<P, Q, PIPES>;
+  constexpr int TT = P::VT / Q;
+  const int grid = bca2_grid<P>(k, PIPES * P::NT, L::BYTES, ((T_ + TT - 1) / TT + PIPES - 1) / PIPES, sms);
+  if (grid <= 0) return false;
+  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_);
+  return true;
+}
+
+// p = 1024 bf16: W spectra in TMEM + staged pipes (bca_fwd5); RDFFT_BCA_FWD5=0 falls back to fwd4.
+inline bool use_fwd5() {
+  static const bool v = [] {
+    const char* e = std::getenv("RDFFT_BCA_FWD5");
+    return !(e && *e == '0');
+  }();
+  return v;
+}
+
+// bf16: the 2-pipe kernel (LLaMA shape 0.190 -> 0.163 ms measured); fp32 keeps the staged
+// single-pipe kernel (its 8-byte direct loads made the 2-pipe variant slower: 0.194 -> 0.205 ms).
+// RDFFT_BCA_FWD4=0 selects the single-pipe kernel for bf16 too, for comparison.
+inline bool use_fwd4() {
+  static const bool v = [] {
+    const char* e = std::getenv("RDFFT_BCA_FWD4");
+    return !(e && *e == '0');
+  }();
+  return v;
+}
+
+#ifndef RDFFT_BCA_FWD_VT
+#define RDFFT_BCA_FWD_VT 16   // p = 1024 forward: 32 vectors (8 tokens of q = 4) per tile, 512 threads
+#endif
+#ifndef RDFFT_BCA_FWD_NSTG
+#define RDFFT_BCA_FWD_NSTG 2  // ... with pass 1 reading x straight from HBM (H + W fill shared memory)
+#endif
+// Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
+template <typename T, int Q>
+bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st) {
+  switch (p) {
+    case 256:
+      if constexpr (sizeof(T) == 2)
+        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 256, 16, 16>, Q, 2>(x, w, y, T_, sms, st);
+      return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
+    case 1024:
+      if constexpr (sizeof(T) == 2) {
+        if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st);
+        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st);
+      }
+      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
+          x, w, y, T_, sms, st);
+    default: return false;
+  }
+}
+template <typename T>
+bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
+  if (q_in != q_out) return false;
+  switch (q_in) {
+    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st);
+    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st);
+    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st);
+    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st);
+    default: return false;
+  }
+}
+
+}  // namespace rdfft

@@ -196,46 +196,4 @@ bool launch_bca_bwd4(const typename P::elem* x, const typename P::elem* w, const
   return true;
 }
 
-// Measured (B200, T = 16384, bf16): LLaMA shape (p = 1024, q = 4) 0.319 -> 0.300 ms, RoBERTa-large
-// (p = 256, q = 4) 0.110 -> 0.097 ms; RoBERTa-base (p = 256, q = 3) 0.073 -> 0.103 ms (kept on bwd2).
-// RDFFT_BCA_BWD4=0 selects the previous kernels (bca_bwd2 / bca_bwd3) for comparison.
-inline bool use_bwd4() {
-  static const bool v = [] {
-    const char* e = std::getenv("RDFFT_BCA_BWD4");
-    return !(e && *e == '0');
-  }();
-  return v;
-}
-
-template <typename T, int Q>
-bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
-                    cudaStream_t st) {
-  const bool v4 = use_bwd4() && Q % 2 == 0;  // odd q: half the pair-split product is predicated off
-  switch (p) {
-    case 256:  // odd q predicates half of the pair-split product: the 2-group kernel measured faster
-      if (v4) return launch_bca_bwd4<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      return launch_bca_bwd2<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-    case 512:
-      if (v4) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st);
-    case 1024:
-      if (v4) return launch_bca_bwd4<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-    default: return false;
-  }
-}
-
-template <typename T>
-bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
-                  int sms, cudaStream_t st) {
-  if (q_in != q_out) return false;
-  switch (q_in) {
-    case 1: return bca_bwd_fast_q<T, 1>(x, w, g, dx, dw, T_, p, sms, st);
-    case 2: return bca_bwd_fast_q<T, 2>(x, w, g, dx, dw, T_, p, sms, st);
-    case 3: return bca_bwd_fast_q<T, 3>(x, w, g, dx, dw, T_, p, sms, st);
-    case 4: return bca_bwd_fast_q<T, 4>(x, w, g, dx, dw, T_, p, sms, st);
-    default: return false;
-  }
-}
-
 }  // namespace rdfft
