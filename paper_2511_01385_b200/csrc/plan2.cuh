@@ -70,6 +70,19 @@ struct sio1<__nv_bfloat16> {
 };
 
 template <typename T>
+struct gio1;  // global single-element loads of T (streaming), widened to fp32 (sio1's interface)
+template <>
+struct gio1<float> {
+  __device__ __forceinline__ static float ld(const float* p, uint32_t) { return __ldcs(p); }
+};
+template <>
+struct gio1<__nv_bfloat16> {
+  __device__ __forceinline__ static float ld(const __nv_bfloat16* p, uint32_t k65536) {
+    return __uint_as_float((uint32_t)__ldcs(reinterpret_cast<const unsigned short*>(p)) * k65536);
+  }
+};
+
+template <typename T>
 struct gio;  // global pair loads / stores (streaming)
 template <>
 struct gio<float> {
@@ -77,6 +90,7 @@ struct gio<float> {
     return __ldcs(reinterpret_cast<const float2*>(p));
   }
   __device__ __forceinline__ static void st2(float* p, float2 v) { __stcs(reinterpret_cast<float2*>(p), v); }
+  __device__ __forceinline__ static void st1(float* p, float v) { __stcs(p, v); }
 };
 template <>
 struct gio<__nv_bfloat16> {
@@ -88,12 +102,21 @@ struct gio<__nv_bfloat16> {
     __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
     __stcs(reinterpret_cast<unsigned int*>(p), *reinterpret_cast<unsigned int*>(&h));
   }
+  __device__ __forceinline__ static void st1(__nv_bfloat16* p, float v) {
+    __nv_bfloat16 h = __float2bfloat16_rn(v);
+    __stcs(reinterpret_cast<unsigned short*>(p), *reinterpret_cast<unsigned short*>(&h));
+  }
 };
 
-template <typename T, int N_, int R_, int VT_, int NSTG_ = 2>
+template <typename T, int N_, int R_, int VT_, int NSTG_ = 2, bool FD_ = false>
 struct Plan2 {
   using elem = T;
   static constexpr int N = N_, R = R_, VT = VT_;
+  // FD: the forward's last pass (and DC lanes) store the packed outputs straight to HBM (one
+  // element per lane) instead of H + a chunked store phase.  Off for every plan2 shape: a warp
+  // then stores 16 consecutive slots of each of two rows per instruction, measured 0.65 -> 0.33
+  // of HBM at bf16 n = 256 and 0.72 -> 0.56 at n = 1024 (plan3, 32 slots of one row, gains).
+  static constexpr bool FD = FD_;
   static constexpr int NSTG = NSTG_;  // staging buffers (TMA ring depth) of the stand-alone transforms
   static constexpr int LN = ilog2c<N>();
   static constexpr int LR = ilog2c<R>();
@@ -116,7 +139,7 @@ struct Plan2 {
   // staged rows are skewed by 64 bytes: the two vectors of a warp read complementary bank halves
   static constexpr int SROW = N + 64 / (int)sizeof(T);
   static constexpr int STAGE = VT * SROW * (int)sizeof(T);
-  static_assert(M <= R && M >= 4 && (R == 32 || R == 16), "2-pass plan shape");
+  static_assert(M <= 2 * R && M >= 4 && (R == 64 || R == 32 || R == 16), "2-pass plan shape");
   static_assert(NT % 32 == 0 && VT * P1 <= NT, "thread mapping");
   static_assert(VT <= 32, "one DC-set lane per vector in the last warp");
   static_assert((VT * CHV) % NT == 0, "chunk mapping");
@@ -277,6 +300,72 @@ __device__ __forceinline__ void p2_dc_fwd(const P2Roles<P>& r, int nv) {
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
       r.hd[jj * WSTR] = make_float2(d[jj], d[jj + M / 2]);
+    });
+  }
+}
+
+// Forward last pass / DC set writing the packed outputs straight to the global tile (P::FD):
+// the slots p2_last_fwd / p2_dc_fwd would write into H, in natural order.
+template <typename P>
+__device__ __forceinline__ void p2_last_fwd_direct(const P2Roles<P>& r, typename P::elem* dst, int nv) {
+  using T = typename P::elem;
+  constexpr int M = P::M, WSTR = P::WSTR, R = P::R, N = P::N;
+  if (r.v2 < nv) {
+    float zr[M], zi[M];
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      const float2 a = r.ha[jj * WSTR];
+      const float2 bb = r.hmz[jj * WSTR];
+      zr[jj] = a.x;
+      zr[jj + M / 2] = a.y;
+      zi[jj] = bb.x;
+      zi[jj + M / 2] = bb.y;
+    });
+    ct::static_for<0, M / 2>([&](auto J2) {
+      constexpr int j0 = 2 * decltype(J2)::value;
+      const float4 t2 = *reinterpret_cast<const float4*>(r.twf + j0);
+      if constexpr (j0 > 0) {
+        const float q = zr[j0];
+        zr[j0] = fmaf(q, t2.x, -zi[j0] * t2.y);
+        zi[j0] = fmaf(q, t2.y, zi[j0] * t2.x);
+      }
+      const float q1 = zr[j0 + 1];
+      zr[j0 + 1] = fmaf(q1, t2.z, -zi[j0 + 1] * t2.w);
+      zi[j0 + 1] = fmaf(q1, t2.w, zi[j0 + 1] * t2.z);
+    });
+    cfft_dit<M>(zr, zi);
+    T* da = dst + r.v2 * N + r.k;        // slots q R + k (and + N/2)
+    T* dm = dst + r.v2 * N + (R - r.k);  // slots q R + R - k
+    ct::static_for<0, M / 2>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      gio<T>::st1(da + q * R, zr[q]);
+      gio<T>::st1(da + q * R + N / 2, -zi[q + M / 2]);
+      if (!r.kz) {  // k = R/2: the mirror slot is the same slot (written from the ascending side)
+        gio<T>::st1(dm + (M / 2 - 1 - q) * R, zr[q + M / 2]);
+        gio<T>::st1(dm + (M / 2 - 1 - q) * R + N / 2, zi[q]);
+      }
+    });
+  }
+}
+
+template <typename P>
+__device__ __forceinline__ void p2_dc_fwd_direct(const P2Roles<P>& r, typename P::elem* dst, int nv) {
+  using T = typename P::elem;
+  constexpr int M = P::M, WSTR = P::WSTR, R = P::R, N = P::N;
+  if (r.dv >= 0 && r.dv < nv) {
+    float d[M];
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      const float2 a = r.hd[jj * WSTR];
+      d[jj] = a.x;
+      d[jj + M / 2] = a.y;
+    });
+    rfft_fwd_reg<M>(d);
+    T* dd = dst + r.dv * N;
+    ct::static_for<0, M / 2>([&](auto J) {
+      constexpr int jj = decltype(J)::value;
+      gio<T>::st1(dd + jj * R, d[jj]);
+      gio<T>::st1(dd + jj * R + N / 2, d[jj + M / 2]);
     });
   }
 }
@@ -473,10 +562,15 @@ __global__ void __launch_bounds__(P::NTT) rdfft2_kernel(typename P::elem* __rest
     if constexpr (NS == 0) {  // forward without staging: pass 1 loads straight from HBM
       p2_pass1_fwd<P, true>(r, xt, nv, k65536);
       __syncthreads();
-      p2_last_fwd<P>(r, nv);
-      p2_dc_fwd<P>(r, nv);
-      __syncthreads();
-      p2_store<P>(r, xt, nv);
+      if constexpr (P::FD) {
+        p2_last_fwd_direct<P>(r, xt, nv);
+        p2_dc_fwd_direct<P>(r, xt, nv);
+      } else {
+        p2_last_fwd<P>(r, nv);
+        p2_dc_fwd<P>(r, nv);
+        __syncthreads();
+        p2_store<P>(r, xt, nv);
+      }
     } else {
       const int sb = it % NS;
       const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
@@ -486,10 +580,15 @@ __global__ void __launch_bounds__(P::NTT) rdfft2_kernel(typename P::elem* __rest
         p2_pass1_fwd<P>(r, st, nv, k65536);
         __syncthreads();  // H complete; staging buffer sb consumed
         if (tid == 0 && nxt < ntiles) stage_issue_rows<P>(x + nxt * VT * (int64_t)N, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
-        p2_last_fwd<P>(r, nv);
-        p2_dc_fwd<P>(r, nv);
-        __syncthreads();
-        if (P::NTT == P::NT || tid < P::NT) p2_store<P>(r, xt, nv);
+        if constexpr (P::FD) {
+          p2_last_fwd_direct<P>(r, xt, nv);
+          p2_dc_fwd_direct<P>(r, xt, nv);
+        } else {
+          p2_last_fwd<P>(r, nv);
+          p2_dc_fwd<P>(r, nv);
+          __syncthreads();
+          if (P::NTT == P::NT || tid < P::NT) p2_store<P>(r, xt, nv);
+        }
       } else {
         p2_load<P>(r, st, nv, k65536);
         __syncthreads();

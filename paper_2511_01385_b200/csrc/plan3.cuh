@@ -8,6 +8,12 @@
 // regrouped as "twiddle + small complex DIT FFT" on a Prop. 1 closed set; the
 // block DCs of each pass form a real FFT run by dedicated lanes.  The shared
 // layout (padded 32-slot windows, half pairs, row skew) is plan2's.
+// The forward's last pass stores its outputs straight to HBM (Plan3::FD: a warp covers 32
+// consecutive slots of one row per 2-byte / 4-byte store), which drops the H -> HBM store phase
+// and one barrier: bf16 n = 2048 fwd 0.55 -> 0.59 of HBM, 4096 0.50 -> 0.53, fp32 2048
+// 0.81 -> 0.88, 4096 0.72 -> 0.74 (profiles/r01_v13_sweep.jsonl).
+// NSTG = 0 (pass 1 / the inverse's first pass reading HBM directly, 5 CTAs/SM instead of 4) is
+// supported but measured slower for every (n, dtype): bf16 4096 0.53 -> 0.47, fp32 2048 0.92 -> 0.69.
 #pragma once
 
 #include "plan2.cuh"
@@ -17,10 +23,11 @@
 
 namespace rdfft {
 
-template <typename T, int N_, int VT_, int NSTG_ = 2>
+template <typename T, int N_, int VT_, int NSTG_ = 2, bool FD_ = false>
 struct Plan3 {
   using elem = T;
   static constexpr int N = N_, VT = VT_, R = 32, NSTG = NSTG_;
+  static constexpr bool FD = FD_;  // forward last pass stores straight to HBM (see Plan2::FD)
   static constexpr int M2 = 4, W2 = 128;     // middle pass
   static constexpr int M3 = N / W2, LM3 = ilog2c<M3>();
   static constexpr int LR = 5, S = N / R, LS = ilog2c<S>(), P1 = S / 2;
@@ -54,7 +61,7 @@ struct P3Smem {  // [stage 0][stage 1][H][TWm][TWl][bars]
   static constexpr size_t TWM_OFF = H_OFF + (size_t)P::HF * 8;
   static constexpr size_t TWL_OFF = TWM_OFF + (size_t)P::TWM * 8;
   static constexpr size_t BAR_OFF = TWL_OFF + (size_t)P::TWL * 8;
-  static constexpr size_t BYTES = BAR_OFF + 8 * P::NSTG;
+  static constexpr size_t BYTES = BAR_OFF + 8 * (P::NSTG > 0 ? P::NSTG : 1);
 };
 
 // Middle-pass general set on both half-pair lanes: Z_j(k), j < 4, of one 128-slot window.
@@ -195,19 +202,70 @@ __device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2
   }
 }
 
+// Forward last-pass set storing its packed outputs straight to the global row (Plan3::FD):
+// da -> slot k of the row, dm -> slot 128 - k; kz: k = 64, whose mirror slot is its own.
+template <int M, typename T>
+__device__ __forceinline__ void p3_last_set_fwd_direct(const float2* ha, const float2* hmi, const LTw& tw, T* da,
+                                                       T* dm, bool kz, int n) {
+  constexpr int WS = 4 * 34, LM = ilog2c<M>();
+  float zr[M], zi[M];
+  ct::static_for<0, M / 2>([&](auto J) {
+    constexpr int jj = decltype(J)::value;
+    const float2 a = ha[jj * WS], b = hmi[jj * WS];
+    zr[jj] = a.x; zr[jj + M / 2] = a.y;
+    zi[jj] = b.x; zi[jj + M / 2] = b.y;
+  });
+  ct::static_for<1, M>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    const float2 t = tw.template at<rev_bits<LM>(j)>();
+    const float q = zr[j];
+    zr[j] = fmaf(q, t.x, -zi[j] * t.y);
+    zi[j] = fmaf(q, t.y, zi[j] * t.x);
+  });
+  cfft_dit<M>(zr, zi);
+  ct::static_for<0, M / 2>([&](auto Q) {
+    constexpr int q = decltype(Q)::value;
+    gio<T>::st1(da + q * 128, zr[q]);
+    gio<T>::st1(da + q * 128 + n / 2, -zi[q + M / 2]);
+    if (!kz) {
+      gio<T>::st1(dm + (M / 2 - 1 - q) * 128, zr[q + M / 2]);
+      gio<T>::st1(dm + (M / 2 - 1 - q) * 128 + n / 2, zi[q]);
+    }
+  });
+}
+
+// Forward last-pass DC set (slots j 128, j 128 + n/2) from H, stored straight to the global row.
+template <int M, typename T>
+__device__ __forceinline__ void p3_dc_fwd_direct(const float2* hd, T* d0, int n) {
+  constexpr int WS = 4 * 34;
+  float d[M];
+  ct::static_for<0, M / 2>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    const float2 a = hd[j * WS];
+    d[j] = a.x;
+    d[j + M / 2] = a.y;
+  });
+  rfft_fwd_reg<M>(d);
+  ct::static_for<0, M / 2>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    gio<T>::st1(d0 + j * 128, d[j]);
+    gio<T>::st1(d0 + j * 128 + n / 2, d[j + M / 2]);
+  });
+}
+
 // Inverse last-pass set read straight from the staged tile (natural order, element type T): the
 // values p3_last_set<M, true> would read from H after the load phase copied them there.
-template <int M, typename T>
+template <int M, typename T, typename LD = sio1<T>>
 __device__ __forceinline__ void p3_last_set_inv_st(const T* sa, const T* sm, float2* ha, float2* hmo, const LTw& tw,
                                                    int n, uint32_t k65536) {
   constexpr int WS = 4 * 34, LM = ilog2c<M>();
   float zr[M], zi[M];
   ct::static_for<0, M / 2>([&](auto Q) {
     constexpr int q = decltype(Q)::value;
-    zr[rev_bits<LM>(q)] = sio1<T>::ld(sa + q * 128, k65536);
-    zi[rev_bits<LM>(q + M / 2)] = -sio1<T>::ld(sa + q * 128 + n / 2, k65536);
-    zr[rev_bits<LM>(q + M / 2)] = sio1<T>::ld(sm + (M / 2 - 1 - q) * 128, k65536);
-    zi[rev_bits<LM>(q)] = sio1<T>::ld(sm + (M / 2 - 1 - q) * 128 + n / 2, k65536);
+    zr[rev_bits<LM>(q)] = LD::ld(sa + q * 128, k65536);
+    zi[rev_bits<LM>(q + M / 2)] = -LD::ld(sa + q * 128 + n / 2, k65536);
+    zr[rev_bits<LM>(q + M / 2)] = LD::ld(sm + (M / 2 - 1 - q) * 128, k65536);
+    zi[rev_bits<LM>(q)] = LD::ld(sm + (M / 2 - 1 - q) * 128 + n / 2, k65536);
   });
   cfft_dit<M, true>(zr, zi);
   ct::static_for<0, M>([&](auto J) {
@@ -227,14 +285,14 @@ __device__ __forceinline__ void p3_last_set_inv_st(const T* sa, const T* sm, flo
 }
 
 // Inverse last-pass DC set from the staged tile: slots j 128 and j 128 + n/2 -> H half pairs.
-template <int M, typename T>
+template <int M, typename T, typename LD = sio1<T>>
 __device__ __forceinline__ void p3_dc_inv_st(const T* s, float2* hd, int n, uint32_t k65536) {
   constexpr int WS = 4 * 34;
   float d[M];
   ct::static_for<0, M / 2>([&](auto J) {
     constexpr int j = decltype(J)::value;
-    d[j] = sio1<T>::ld(s + j * 128, k65536);
-    d[j + M / 2] = sio1<T>::ld(s + j * 128 + n / 2, k65536);
+    d[j] = LD::ld(s + j * 128, k65536);
+    d[j + M / 2] = LD::ld(s + j * 128 + n / 2, k65536);
   });
   rfft_inv_reg<M>(d);
   const float sc = 1.0f / (float)n;
@@ -304,7 +362,7 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
     pad[1] = make_float2(0.f, 0.f);
   }
   if (tid == 0) {
-    for (int q = 0; q < P::NSTG; ++q) mbar_init(bar + q, 1);
+    for (int q = 0; q < (P::NSTG > 0 ? P::NSTG : 1); ++q) mbar_init(bar + q, 1);
     fence_mbar_init();
   }
   // ---- roles
@@ -384,31 +442,36 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
     });
     if (dcl >= 0 && dcl < nv) p3_dc_set<P::M3, 4 * WS, kInv, float>(lhd, kInv ? 1.0f / N : 1.0f);
   };
-  auto last_inv_st = [&](const T* st, int nv) {  // the inverse's first pass, reading the staged tile
+  // the inverse's first pass, reading the staged tile (NSTG > 0) or the global tile (NSTG = 0)
+  using LD = std::conditional_t<(P::NSTG > 0), sio1<T>, gio1<T>>;
+  auto last_inv_st = [&](const T* st, int nv) {
     ct::static_for<0, LITEMS>([&](auto RR) {
       constexpr int r = decltype(RR)::value;
       constexpr int dv = r * LSTEP;
       constexpr int off = dv * P::ROWA + 2 * dv;
       const T* sv = st + (vl0 + dv) * N;
-      if (vl0 + dv < nv) p3_last_set_inv_st<P::M3, T>(sv + qa, sv + qm, lha + off, lhz + off, ltw, N, k65536);
+      if (vl0 + dv < nv) p3_last_set_inv_st<P::M3, T, LD>(sv + qa, sv + qm, lha + off, lhz + off, ltw, N, k65536);
     });
-    if (dcl >= 0 && dcl < nv) p3_dc_inv_st<P::M3, T>(st + dcl * N, lhd, N, k65536);
+    if (dcl >= 0 && dcl < nv) p3_dc_inv_st<P::M3, T, LD>(st + dcl * N, lhd, N, k65536);
   };
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int nv = (int)(batch - tile * VT < VT ? batch - tile * VT : VT);
     T* xt = x + tile * VT * (int64_t)N;
-    const int sb = it % NS;
-    const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
+    const int sb = NS > 0 ? it % NS : 0;
+    const T* st = NS > 0 ? reinterpret_cast<const T*>(base + sb * P::STAGE) : xt;
     const int64_t nxt = tile + NS * (int64_t)gridDim.x;
-    mbar_wait(bar + sb, (it / NS) & 1);
+    if constexpr (NS > 0) mbar_wait(bar + sb, (it / NS) & 1);
     if (!kInv) {
       if (v1 < nv) {  // pass 1 (plan2's)
         float2 b[R];
         const T* src = st + s1;
         ct::static_for<0, R>([&](auto I) {
           constexpr int i = decltype(I)::value;
-          b[rev_bits<P::LR>(i)] = sio<T>::ld2(src + S * i, k65536);
+          if constexpr (NS > 0)
+            b[rev_bits<P::LR>(i)] = sio<T>::ld2(src + S * i, k65536);
+          else
+            b[rev_bits<P::LR>(i)] = gio<T>::ld2(src + S * i, k65536);
         });
         rfft_fwd_reg<R>(b);
         ct::static_for<0, R / 2>([&](auto I) {
@@ -417,9 +480,19 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
         });
       }
       __syncthreads();
-      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+      if (NS > 0 && tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
       middle(nv);
       __syncthreads();
+      if constexpr (P::FD) {
+        ct::static_for<0, LITEMS>([&](auto RR) {
+          constexpr int r = decltype(RR)::value;
+          constexpr int dv = r * LSTEP;
+          constexpr int off = dv * P::ROWA + 2 * dv;
+          T* xv = xt + (vl0 + dv) * N;
+          if (vl0 + dv < nv) p3_last_set_fwd_direct<P::M3, T>(lha + off, lhz + off, ltw, xv + qa, xv + qm, kl == P::KL, N);
+        });
+        if (dcl >= 0 && dcl < nv) p3_dc_fwd_direct<P::M3, T>(lhd, xt + dcl * N, N);
+      } else {
       last(nv);
       __syncthreads();
       ct::static_for<0, VT * P::CHV / NT>([&](auto RR) {  // store
@@ -432,10 +505,11 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
           gio<T>::st2(d + N / 2, make_float2(f.y, f.w));
         }
       });
+      }
     } else {
       last_inv_st(st, nv);  // reads the staged tile directly (no staged -> H copy)
       __syncthreads();
-      if (tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
+      if (NS > 0 && tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
       middle(nv);
       __syncthreads();
       if (v1 < nv) {  // inverse pass 1
@@ -525,8 +599,8 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
     case 256: return launch_p2<T, 256, 16, 16>(x, batch, inverse, sms, st);
     case 512: return launch_p2<T, 512, 32, 8>(x, batch, inverse, sms, st);
     case 1024: return launch_p2<T, 1024, 32, 8>(x, batch, inverse, sms, st);
-    case 2048: return launch_plan3<Plan3<T, 2048, 4, 1>>(x, batch, inverse, sms, st);
-    case 4096: return launch_plan3<Plan3<T, 4096, 2, 1>>(x, batch, inverse, sms, st);
+    case 2048: return launch_plan3<Plan3<T, 2048, 4, 1, true>>(x, batch, inverse, sms, st);
+    case 4096: return launch_plan3<Plan3<T, 4096, 2, 1, true>>(x, batch, inverse, sms, st);
     case 8192: return launch_planl<PlanL<T, 8192>>(x, batch, inverse, sms, st);
     case 16384: return launch_planl<PlanL<T, 16384>>(x, batch, inverse, sms, st);
     case 32768: return launch_planl<PlanL<T, 32768>>(x, batch, inverse, sms, st);
