@@ -136,8 +136,13 @@ struct Plan2 {
   static constexpr int CHV = N / 4;         // 16-byte H chunks per vector
   static constexpr int DC0 = NT - 32;       // first thread of the warp whose lanes run the DC sets
   static constexpr int NTT = NT;            // threads per CTA (Plan2o adds a dedicated DC warp)
-  // staged rows are skewed by 64 bytes: the two vectors of a warp read complementary bank halves
-  static constexpr int SROW = N + 64 / (int)sizeof(T);
+  // Staged rows are skewed so that the vectors one pass-1 load instruction touches read disjoint
+  // banks: each vector's P1 lanes read P1 x 4 B (bf16 pairs) or P1 x 8 B (float2), so the skew is
+  // that width (capped at 64 B: two vectors per 128-byte wavefront or fewer).  n = 1024: 64 B (two
+  // vectors per warp, complementary bank halves); bf16 n = 256 / 512: 32 B (four vectors per warp).
+  static constexpr int SKEWB_ = (int)(P1 * (sizeof(T) == 2 ? 4 : 8));
+  static constexpr int SKEWB = SKEWB_ < 64 ? SKEWB_ : 64;
+  static constexpr int SROW = N + SKEWB / (int)sizeof(T);
   static constexpr int STAGE = VT * SROW * (int)sizeof(T);
   static_assert(M <= 2 * R && M >= 4 && (R == 64 || R == 32 || R == 16), "2-pass plan shape");
   static_assert(NT % 32 == 0 && VT * P1 <= NT, "thread mapping");
