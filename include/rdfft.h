@@ -13,10 +13,12 @@
  *  - dtype is RDFFT_F32 (IEEE fp32) or RDFFT_BF16 (bfloat16 storage).  All
  *    arithmetic is fp32 in registers; bf16 results are rounded to nearest even
  *    on store (reading C7).  dw is always fp32.
- *  - n (the transform length) is a power of two with 2 <= n <= 32768; the BCA
+ *  - n (the transform length) is a power of two with 2 <= n <= 65536; the BCA
  *    block size p is a power of two with 2 <= p <= 4096 (reading C9; the paper
- *    runs p = 128 .. 4096; n = 8192 .. 32768 is SURVEY
- *    §8(f) N2, one vector per CTA in shared memory).
+ *    runs p = 128 .. 4096; n = 8192 .. 65536 is SURVEY
+ *    §8(f) N2: one vector per CTA in shared memory up to 32768, n = 65536 on a
+ *    thread-block cluster of two CTAs exchanging the last stage through
+ *    distributed shared memory).
  *  - stream is a cudaStream_t (NULL = legacy default stream).  Calls are
  *    asynchronous on that stream; inputs are validated synchronously on the
  *    host before anything is launched, and nothing is launched on error.
@@ -51,7 +53,7 @@ typedef enum { RDFFT_F32 = 0, RDFFT_BF16 = 1 } rdfft_dtype_t;
 
 typedef enum {
   RDFFT_OK = 0,
-  RDFFT_E_SIZE = 1,  /* n not a power of two in [2, 32768] (p: [2, 4096])        */
+  RDFFT_E_SIZE = 1,  /* n not a power of two in [2, 65536] (p: [2, 4096])        */
   RDFFT_E_NULL = 2,  /* null pointer with a non-empty batch                       */
   RDFFT_E_ALIGN = 3, /* a base pointer is not 16-byte aligned                     */
   RDFFT_E_DTYPE = 4, /* dtype not RDFFT_F32 / RDFFT_BF16                          */

@@ -25,8 +25,8 @@ int ilog2(int64_t n) {
   return l;
 }
 // BCA blocks: 2 <= p <= 4096 (reading C9); transforms, packed products and the utilities also
-// take the large sizes of SURVEY §8(f) N2, n <= 32768 (planl.cuh).
-constexpr int64_t kMaxTransformN = 32768;
+// take the large sizes of SURVEY §8(f) N2, n <= 65536 (planl.cuh; 65536 on cluster pairs).
+constexpr int64_t kMaxTransformN = 65536;
 bool pow2_in_range(int64_t n) { return n >= 2 && n <= kMaxN && (n & (n - 1)) == 0; }
 bool pow2_transform(int64_t n) { return n >= 2 && n <= kMaxTransformN && (n & (n - 1)) == 0; }
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -402,7 +402,7 @@ int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* 
 const char* rdfft_status_str(int status) {
   switch (status) {
     case RDFFT_OK: return "ok";
-    case RDFFT_E_SIZE: return "n is not a power of two in [2, 32768] (BCA block p: [2, 4096])";
+    case RDFFT_E_SIZE: return "n is not a power of two in [2, 65536] (BCA block p: [2, 4096])";
     case RDFFT_E_NULL: return "null pointer";
     case RDFFT_E_ALIGN: return "pointer not 16-byte aligned";
     case RDFFT_E_DTYPE: return "unsupported dtype";

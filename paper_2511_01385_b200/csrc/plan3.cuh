@@ -606,6 +606,7 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
     case 8192: return launch_planl<PlanL<T, 8192>>(x, batch, inverse, sms, st);
     case 16384: return launch_planl<PlanL<T, 16384>>(x, batch, inverse, sms, st);
     case 32768: return launch_planl<PlanL<T, 32768>>(x, batch, inverse, sms, st);
+    case 65536: return launch_planl_pair<PlanL<T, 32768>>(x, batch, inverse, sms, st);
     default: return false;
   }
 }

@@ -18,7 +18,18 @@
 // (simulated: <= 1.5 wavefronts per ideal one).  Twiddle tables in shared memory:
 // TW2[j][k-1] = W_1024^{k rev5(j)} (4 KB) and TW3[a][k-1] = W_n^{4 k a} (M3/4 x 512) with
 // W_n^{k b}, b < 4, in registers.  No global scratch.
+//
+// n = 65536 (NC = 2): a thread-block cluster of two CTAs (one per SM, DSMEM between them).  By the
+// per-stage invariant (DIT), after log2(n/2) stages window r in {0, 1} of the vector holds the
+// packed n/2-point spectrum of x[r :: 2], so CTA r runs the n/2 = 32768 plan above on x[r :: 2]
+// (strided loads) into its own shared memory; the last stage (m = n/2, beta = 0: Prop. 1's groups
+// {k, m - k, m + k, 2m - k}) reads one half pair from each CTA (the peer's through
+// ld.shared::cluster) and stores the four outputs straight to HBM.  The inverse runs Eq. 7's first
+// stage (m = n/2, with its 1/2) from HBM into both CTAs' shared memory (the peer's half through
+// st.shared::cluster), then each CTA the exact n/2-point inverse with strided stores.
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "plan2.cuh"
 
@@ -41,7 +52,12 @@ struct PlanL {
   static constexpr int TW2N = 32 * 16, TW3N = (M3 / 4) * K3;
   static constexpr size_t TW2_OFF = (size_t)N * 4;
   static constexpr size_t TW3_OFF = TW2_OFF + (size_t)TW2N * 8;
-  static constexpr size_t BYTES = TW3_OFF + (size_t)TW3N * 8;
+  static constexpr size_t BYTES1 = TW3_OFF + (size_t)TW3N * 8;
+  // cluster pair (n = 2N): cross-stage twiddles W_{2N}^{128 a} (a < N / 256) and W_{2N}^b (b < 128)
+  static constexpr int TWCA = N / 256, TWCB = 128;
+  static constexpr size_t TWC_OFF = BYTES1;
+  static constexpr size_t BYTES2 = TWC_OFF + (size_t)(TWCA + TWCB) * 8;
+  static constexpr size_t BYTES = BYTES1;
   static_assert(M3 >= 8 && M3 <= 32 && LS >= 8, "plan L shape");
   __host__ __device__ static constexpr int swz(int w) { return ((w >> (LS - 4)) ^ (((w >> 5) & 1) << 2)) & 7; }
   // float index of packed slot s
@@ -179,10 +195,71 @@ struct gio4<__nv_bfloat16> {
   }
 };
 
-template <typename P, bool kInv>
+// Cluster-pair cross stage (m = N, the vector has 2N slots), forward: groups k in this CTA's
+// quarter, A from window 0 (H0), B from window 1 (H1), outputs straight to the global row xv.
+template <typename P>
+__device__ __forceinline__ void pl_cross_fwd(const float* H0, const float* H1, const float2* TWCa, float2 twb,
+                                             typename P::elem* xv, int r, int tid) {
+  using T = typename P::elem;
+  constexpr int m = P::N, NT = P::NT, Q = m / 4;
+#pragma unroll 2
+  for (int i = 0; i < Q / NT; ++i) {
+    const int k = r * Q + tid + NT * i;
+    if (k == 0) {  // k = 0: (a, b) -> (a + b, a - b); k = m/2: slot m/2 kept, slot 3m/2 negated
+      const float a = H0[P::phys(0)], b = H1[P::phys(0)];
+      gio<T>::st1(xv, a + b);
+      gio<T>::st1(xv + m, a - b);
+      gio<T>::st1(xv + m / 2, H0[P::phys(m / 2)]);
+      gio<T>::st1(xv + 3 * m / 2, -H1[P::phys(m / 2)]);
+      continue;
+    }
+    const float2 ta = TWCa[k >> 7];  // W_{2m}^k = W^{128 a} W^b, b = k % 128 (fixed per thread)
+    const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
+    const float ar = H0[P::phys(k)], ai = H0[P::phys(m - k)];
+    const float br = H1[P::phys(k)], bi = H1[P::phys(m - k)];
+    const float ur = fmaf(br, wr, -bi * wi), ui = fmaf(br, wi, bi * wr);
+    gio<T>::st1(xv + k, ar + ur);
+    gio<T>::st1(xv + 2 * m - k, ai + ui);
+    gio<T>::st1(xv + m - k, ar - ur);
+    gio<T>::st1(xv + m + k, ui - ai);
+  }
+}
+
+// Cluster-pair cross stage, inverse (Eq. 7's first stage, with its 1/2): global row -> H0, H1.
+template <typename P>
+__device__ __forceinline__ void pl_cross_inv(float* H0, float* H1, const float2* TWCa, float2 twb,
+                                             const typename P::elem* xv, int r, int tid, uint32_t k65536) {
+  using T = typename P::elem;
+  constexpr int m = P::N, NT = P::NT, Q = m / 4;
+#pragma unroll 2
+  for (int i = 0; i < Q / NT; ++i) {
+    const int k = r * Q + tid + NT * i;
+    if (k == 0) {
+      const float s = gio1<T>::ld(xv, k65536), d = gio1<T>::ld(xv + m, k65536);
+      H0[P::phys(0)] = 0.5f * (s + d);
+      H1[P::phys(0)] = 0.5f * (s - d);
+      H0[P::phys(m / 2)] = gio1<T>::ld(xv + m / 2, k65536);
+      H1[P::phys(m / 2)] = -gio1<T>::ld(xv + 3 * m / 2, k65536);
+      continue;
+    }
+    const float2 ta = TWCa[k >> 7];  // conj(W_{2m}^k)
+    const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
+    const float ykr = gio1<T>::ld(xv + k, k65536), yki = gio1<T>::ld(xv + 2 * m - k, k65536);
+    const float ymr = gio1<T>::ld(xv + m - k, k65536), ymi = -gio1<T>::ld(xv + m + k, k65536);
+    const float dr = 0.5f * (ykr - ymr), di = 0.5f * (yki - ymi);
+    H0[P::phys(k)] = 0.5f * (ykr + ymr);
+    H0[P::phys(m - k)] = 0.5f * (yki + ymi);
+    H1[P::phys(k)] = fmaf(dr, wr, -di * wi);
+    H1[P::phys(m - k)] = fmaf(dr, wi, di * wr);
+  }
+}
+
+// NC = 1: one vector of n = N per CTA.  NC = 2: one vector of n = 2N per cluster pair (see header).
+template <typename P, bool kInv, int NC = 1>
 __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem* __restrict__ x, int64_t batch) {
   using T = typename P::elem;
   constexpr int N = P::N, NT = P::NT, R = P::R, S = P::S, K3 = P::K3, M3 = P::M3;
+  static_assert(NC == 1 || NC == 2, "cluster size");
   extern __shared__ float4 smem4[];
   unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
   float* H = reinterpret_cast<float*>(base);
@@ -190,6 +267,26 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   float2* TW3 = reinterpret_cast<float2*>(base + P::TW3_OFF);
   const int tid = threadIdx.x;
   const float sg = kInv ? 1.0f : -1.0f;
+  // cluster pair: rank r holds window r (the n/2-point spectrum of x[r :: 2]); the peer's H via DSMEM
+  const int r = NC == 2 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  float* Hpeer = H;
+  float2* TWCa = reinterpret_cast<float2*>(base + P::TWC_OFF);
+  float2 twb = make_float2(1.f, 0.f);
+  if constexpr (NC == 2) {
+    Hpeer = cooperative_groups::this_cluster().map_shared_rank(H, r ^ 1);
+    for (int e = tid; e < P::TWCA; e += NT) {
+      float s, c;
+      sincospif(2.0f * (float)(128 * e) / (float)(2 * N), &s, &c);
+      TWCa[e] = make_float2(c, sg * s);
+    }
+    float s, c;
+    sincospif(2.0f * (float)(tid % 128) / (float)(2 * N), &s, &c);
+    twb = make_float2(c, sg * s);
+  }
+  float* H0 = r == 0 ? H : Hpeer;
+  float* H1 = r == 0 ? Hpeer : H;
+  constexpr int64_t NV = (int64_t)N * NC;  // elements per vector
+  constexpr int XS = NC;                   // element stride of this CTA's half in the row
   for (int e = tid; e < P::TW2N; e += NT) {
     const int j = e / 16, k = 1 + e % 16;
     float s, c;
@@ -204,16 +301,15 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   }
   // pass-3 sets k3 = tid + NT i (i < K3PT); k3 = 0 stands for the zero-imaginary set k3 = 512
   // plus the DC set (two real-input sets ~ one complex set of work)
-  auto tw3_for = [&](int k3) {
+  auto tw3_for = [&](int k3) {  // W^{k}: one sincospif; W^{2k}, W^{3k} by products (~2-3 ulp)
     LTw3<K3> t;
     t.h = TW3 + (k3 - 1);
     float s, c;
     sincospif(2.0f * (float)k3 / (float)N, &s, &c);
-    t.w1 = make_float2(c, sg * s);
-    sincospif(4.0f * (float)k3 / (float)N, &s, &c);
-    t.w2 = make_float2(c, sg * s);
-    sincospif(6.0f * (float)k3 / (float)N, &s, &c);
-    t.w3 = make_float2(c, sg * s);
+    const float2 w = make_float2(c, sg * s);
+    t.w1 = w;
+    t.w2 = make_float2(fmaf(w.x, w.x, -w.y * w.y), 2.0f * w.x * w.y);
+    t.w3 = make_float2(fmaf(t.w2.x, w.x, -t.w2.y * w.y), fmaf(t.w2.x, w.y, t.w2.y * w.x));
     return t;
   };
   auto pass3 = [&](auto inv) {
@@ -232,15 +328,21 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   tw2.h = TW2 + (k2 - 1);
   const uint32_t k65536 = kTwo16;
   __syncthreads();
-  for (int64_t v = blockIdx.x; v < batch; v += gridDim.x) {
-    T* xv = x + v * (int64_t)N;
+  if constexpr (NC == 2) cooperative_groups::this_cluster().sync();  // peer's H mapped and live
+  for (int64_t v = blockIdx.x / NC; v < batch; v += gridDim.x / NC) {
+    T* xv = x + v * NV;
+    T* xh = xv + r;  // this CTA's half: elements xh[XS * e], e < N
     if (!kInv) {
       if (tid < S / 2) {  // pass 1: subsequences 2c, 2c+1 -> windows rev(2c), rev(2c) + S/2
         const int c = tid;
         float2 b[R];
         ct::static_for<0, R>([&](auto I) {
           constexpr int i = decltype(I)::value;
-          b[rev_bits<5>(i)] = gio<T>::ld2(xv + 2 * c + S * i, k65536);
+          if constexpr (NC == 1)
+            b[rev_bits<5>(i)] = gio<T>::ld2(xv + 2 * c + S * i, k65536);
+          else
+            b[rev_bits<5>(i)] = make_float2(gio1<T>::ld(xh + XS * (2 * c + S * i), k65536),
+                                            gio1<T>::ld(xh + XS * (2 * c + 1 + S * i), k65536));
         });
         rfft_fwd_reg<R>(b);
         const int w0 = rev_bits<P::LS>(2 * c), w1 = w0 + S / 2;
@@ -255,16 +357,27 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       if (act2 && k2 == 16) pl_dc<P, 32, false>(H, ww * 1024, 32, 1.0f);
       __syncthreads();
       pass3(std::false_type{});
-      __syncthreads();
-      for (int e = tid; e < N / 4; e += NT) {
-        const float4 f = *reinterpret_cast<const float4*>(H + P::phys(4 * e));
-        gio4<T>::st(xv + 4 * e, f);
+      if constexpr (NC == 1) {
+        __syncthreads();
+        for (int e = tid; e < N / 4; e += NT) {
+          const float4 f = *reinterpret_cast<const float4*>(H + P::phys(4 * e));
+          gio4<T>::st(xv + 4 * e, f);
+        }
+        __syncthreads();
+      } else {
+        cooperative_groups::this_cluster().sync();  // both windows complete and visible
+        pl_cross_fwd<P>(H0, H1, TWCa, twb, xv, r, tid);
+        cooperative_groups::this_cluster().sync();  // the peer is done reading this H
       }
-      __syncthreads();
     } else {
-      for (int e = tid; e < N / 4; e += NT)
-        *reinterpret_cast<float4*>(H + P::phys(4 * e)) = gio4<T>::ld(xv + 4 * e);
-      __syncthreads();
+      if constexpr (NC == 1) {
+        for (int e = tid; e < N / 4; e += NT)
+          *reinterpret_cast<float4*>(H + P::phys(4 * e)) = gio4<T>::ld(xv + 4 * e);
+        __syncthreads();
+      } else {
+        pl_cross_inv<P>(H0, H1, TWCa, twb, xv, r, tid, k65536);
+        cooperative_groups::this_cluster().sync();  // both windows written (half of each remotely)
+      }
       pass3(std::true_type{});
       __syncthreads();
       if (act2) pl_set<P, 32, true>(H, ww * 1024, 32, k2, tw2);
@@ -286,10 +399,18 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         rfft_inv_reg<R>(b);
         ct::static_for<0, R>([&](auto I) {
           constexpr int i = decltype(I)::value;
-          gio<T>::st2(xv + 2 * c + S * i, b[rev_bits<5>(i)]);
+          if constexpr (NC == 1) {
+            gio<T>::st2(xv + 2 * c + S * i, b[rev_bits<5>(i)]);
+          } else {
+            gio<T>::st1(xh + XS * (2 * c + S * i), b[rev_bits<5>(i)].x);
+            gio<T>::st1(xh + XS * (2 * c + 1 + S * i), b[rev_bits<5>(i)].y);
+          }
         });
       }
-      __syncthreads();
+      if constexpr (NC == 1)
+        __syncthreads();
+      else
+        cooperative_groups::this_cluster().sync();  // the peer's next cross stage writes this H
     }
   }
 }
@@ -319,6 +440,39 @@ bool launch_planl(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
   else
     kf<<<grid, P::NT, P::BYTES, st>>>(x, batch);
   return true;
+}
+
+// n = 2 N on cluster pairs (P = PlanL<T, N>, N = 32768 -> n = 65536): one pair per 2 SMs.
+template <typename P>
+bool launch_planl_pair(typename P::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
+  auto kf = rdfftl_kernel<P, false, 2>;
+  auto ki = rdfftl_kernel<P, true, 2>;
+  static bool configured = false;
+  if (!configured) {
+    for (auto k : {kf, ki}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::BYTES2);
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    }
+    configured = true;
+    if (verbose())
+      std::fprintf(stderr, "[rdfft] planL pair n=%d: %zu B smem per CTA, %d threads, cluster 2\n", 2 * P::N,
+                   (size_t)P::BYTES2, P::NT);
+  }
+  const int64_t pairs = batch < (int64_t)(sms / 2) ? batch : (int64_t)(sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(P::NT);
+  cfg.dynamicSmemBytes = P::BYTES2;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = inverse ? cudaLaunchKernelEx(&cfg, ki, x, batch) : cudaLaunchKernelEx(&cfg, kf, x, batch);
+  return e == cudaSuccess;
 }
 
 }  // namespace rdfft

@@ -55,7 +55,7 @@ def test_transform_validation(lib):
     for fn in (lib.rdfft_fwd, lib.rdfft_inv):
         assert fn(FAKE, 4, 3, 0, None) == 1        # E_SIZE: not a power of two
         assert fn(FAKE, 4, 1, 0, None) == 1        # E_SIZE: n = 1
-        assert fn(FAKE, 4, 65536, 0, None) == 1    # E_SIZE: above 32768
+        assert fn(FAKE, 4, 131072, 0, None) == 1   # E_SIZE: above 65536
         assert fn(FAKE, 4, 8, 7, None) == 4        # E_DTYPE
         assert fn(FAKE, -1, 8, 0, None) == 5       # E_SHAPE
         assert fn(None, 4, 8, 0, None) == 2        # E_NULL

@@ -236,6 +236,69 @@ def test_large_n_forward_inverse(n, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_cluster_pair_n65536(dtype):
+    """n = 65536 on thread-block cluster pairs (planl.cuh NC = 2: each CTA transforms x[r :: 2],
+    the last stage exchanges through DSMEM).  A batch above the pair count (persistent loop),
+    the forward on one row against the oracle, the inverse through the oracle's forward
+    (oracle_fwd(inv(p)) = p: the DFT is a bijection; the O(n^2) inverse oracle takes minutes here),
+    the round trip on every row, exact impulse / e_0 / e_{n/2} probes and cosine / sine probes on
+    both sides of the CTA split (slot k owned by rank 0 for k < n/8, rank 1 above)."""
+    n, b = 65536, 74 + 3
+    x = synth.randn((b, n), seed=765, dtype=dtype).cuda()
+    x[0].zero_()
+    x[0, 0] = 1
+    x0 = x.clone()
+    xin = f64(x[b - 1 :])
+    R.rdfft_fwd(x)
+    torch.cuda.synchronize()
+    imp = np.zeros(n)
+    imp[: n // 2 + 1] = 1
+    assert np.array_equal(f64(x[0]), imp)
+    assert rel_l2_rows(f64(x[b - 1 :]), o.rdfft_fwd(xin)) <= TOL[dtype]
+    R.rdfft_inv(x)
+    torch.cuda.synchronize()
+    err = (x.float() - x0.float()).norm(dim=1) / x0.float().norm(dim=1)
+    assert float(err.max()) <= (2e-5 if dtype == "f32" else 2e-2)
+    if dtype == "f32":
+        p = synth.randn((1, n), seed=766, dtype=dtype).cuda()
+        pin = f64(p)
+        R.rdfft_inv(p)
+        torch.cuda.synchronize()
+        assert rel_l2_rows(o.rdfft_fwd(f64(p)), pin) <= TOL[dtype]
+    # inverse probes (P2): e_0 -> 1/n, e_{n/2} -> (-1)^t / n exactly; e_k -> (2/n) cos(2 pi k t / n),
+    # e_{n-k} -> -(2/n) sin(2 pi k t / n)
+    ks = [1, 3, n // 8 - 1, n // 8, n // 8 + 5, n // 4 - 1, n // 4 + 1, n // 2 - 1]
+    e = torch.zeros((2 + 2 * len(ks), n), dtype=x.dtype, device="cuda")
+    e[0, 0] = 1
+    e[1, n // 2] = 1
+    for i, k in enumerate(ks):
+        e[2 + 2 * i, k] = 1
+        e[3 + 2 * i, n - k] = 1
+    R.rdfft_inv(e)
+    torch.cuda.synchronize()
+    t = np.arange(n)
+    got = f64(e)
+    assert np.array_equal(got[0], np.full(n, 1.0 / n))
+    assert np.array_equal(got[1], (-1.0) ** t / n)
+    for i, k in enumerate(ks):
+        c = 2.0 / n * np.cos(2 * np.pi * ((k * t) % n) / n)
+        s = -2.0 / n * np.sin(2 * np.pi * ((k * t) % n) / n)
+        assert rel_l2_rows(got[2 + 2 * i], c) <= TOL[dtype], k
+        assert rel_l2_rows(got[3 + 2 * i], s) <= TOL[dtype], k
+    # forward probes: cos at k0 -> slot k0 = n/2, sin at k0 -> slot n - k0 = -n/2 (right slot, sign)
+    f = torch.tensor(np.stack([np.cos(2 * np.pi * ((k * t) % n) / n) for k in ks] +
+                              [np.sin(2 * np.pi * ((k * t) % n) / n) for k in ks]), dtype=torch.float32)
+    f = f.to(x.dtype).cuda()
+    R.rdfft_fwd(f)
+    torch.cuda.synchronize()
+    got = f64(f)
+    for i, k in enumerate(ks):
+        assert int(np.argmax(np.abs(got[i]))) == k and got[i, k] > n / 4
+        j = len(ks) + i
+        assert int(np.argmax(np.abs(got[j]))) == n - k and got[j, n - k] < -n / 4
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("conj", [False, True])
 def test_large_n_packed_mul(dtype, conj):
     n, b = 8192, 7
