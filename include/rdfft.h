@@ -94,6 +94,16 @@ int rdfft_packed_conjmul(void* a, const void* b, int64_t batch, int64_t n, int64
 int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
             int dtype, void* stream);
 
+/* bca_fwd_accum — bca_fwd that ADDS the adapter output to y's contents:
+ *   y <- y + IrdFFT(sum_j W_ij (.) X_j)
+ * i.e. the frozen path's output W0 x (already in y) plus the block-circulant
+ * adapter in the same pass, as the adapter is used in fine-tuning
+ * (SURVEY §8(f) N4 "y += fusion").  y is read and written
+ * once per element (fp32 add, then the usual RNE store for bf16).  Same
+ * arguments and aliasing rules as bca_fwd.                                  */
+int bca_fwd_accum(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
+                  int dtype, void* stream);
+
 /* bca_bwd — fused block-circulant adapter backward (Eq. 5, P:L174-183;
  * blockwise pairing reading C11).  With G_i = rdFFT(g_i), X_j = rdFFT(x_j),
  * W_ij = rdFFT(w_ij):

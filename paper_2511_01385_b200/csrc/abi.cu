@@ -159,7 +159,7 @@ int grid_for(K kernel, int threads, size_t smem, int64_t units) {
 
 
 int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, int q_out, int p, int logp, int dtype,
-                  cudaStream_t st) {
+                  cudaStream_t st, int acc) {
   BcaTiledPlan plan{};
   if (!bca_tiled_plan(false, false, T, q_in, q_out, p, num_sms(), &plan)) return RDFFT_E_SHAPE;
   const dim3 grid((unsigned)std::min<int64_t>(plan.tiles, (int64_t)num_sms() * 4), (unsigned)plan.groups);
@@ -167,14 +167,15 @@ int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, in
     auto k = bca_fwd_tiled_kernel<float>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
     k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
-                                                  static_cast<float*>(y), T, q_in, q_out, p, logp, plan.vt, plan.grp);
+                                                  static_cast<float*>(y), T, q_in, q_out, p, logp, plan.vt, plan.grp,
+                                                  acc);
   } else {
     auto k = bca_fwd_tiled_kernel<__nv_bfloat16>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
     k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<const __nv_bfloat16*>(w),
                                                   static_cast<__nv_bfloat16*>(y), T, q_in, q_out, p, logp, plan.vt,
-                                                  plan.grp);
+                                                  plan.grp, acc);
   }
   return launched();
 }
@@ -269,8 +270,8 @@ int rdfft_packed_conjmul(void* a, const void* b, int64_t batch, int64_t n, int64
   return packed(a, b, batch, n, b_batch, dtype, stream, true);
 }
 
-int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p, int dtype,
-            void* stream) {
+static int bca_fwd_impl(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
+                        int dtype, void* stream, int acc) {
   int rc = bca_check(x, w, T, d_in, d_out, p, dtype);
   if (rc != RDFFT_OK || T == 0) return rc;
   if (!y) return RDFFT_E_NULL;
@@ -282,28 +283,38 @@ int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int6
   const size_t smem = bca_fwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logp = ilog2(p);
-  if (smem > 227 * 1024) return bca_fwd_tiled(x, w, y, T, q_in, q_out, (int)p, logp, dtype, st);
+  if (smem > 227 * 1024) return bca_fwd_tiled(x, w, y, T, q_in, q_out, (int)p, logp, dtype, st, acc);
   const bool fast =
       dtype == RDFFT_F32
           ? bca_fwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w), static_cast<float*>(y), T,
-                                q_in, q_out, (int)p, num_sms(), st)
+                                q_in, q_out, (int)p, num_sms(), st, acc)
           : bca_fwd_fast<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
-                                        static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, num_sms(), st);
+                                        static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, num_sms(), st, acc);
   if (fast) return launched();
   if (dtype == RDFFT_F32) {
     auto k = bca_fwd_v1_kernel<float>;
     const int grid = grid_for(k, kBcaThreads, smem, T);
     if (!grid) return RDFFT_E_SHAPE;
     k<<<grid, kBcaThreads, smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
-                                       static_cast<float*>(y), T, q_in, q_out, (int)p, logp);
+                                       static_cast<float*>(y), T, q_in, q_out, (int)p, logp, acc);
   } else {
     auto k = bca_fwd_v1_kernel<__nv_bfloat16>;
     const int grid = grid_for(k, kBcaThreads, smem, T);
     if (!grid) return RDFFT_E_SHAPE;
     k<<<grid, kBcaThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
-                                       static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, logp);
+                                       static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, logp, acc);
   }
   return launched();
+}
+
+int bca_fwd(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p, int dtype,
+            void* stream) {
+  return bca_fwd_impl(x, w, y, T, d_in, d_out, p, dtype, stream, 0);
+}
+
+int bca_fwd_accum(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
+                  int dtype, void* stream) {
+  return bca_fwd_impl(x, w, y, T, d_in, d_out, p, dtype, stream, 1);
 }
 
 static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,

@@ -141,7 +141,8 @@ __device__ __forceinline__ void bca_product_fwd(float2* H, const float2* Wr, int
 template <typename P, int Q>
 __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::elem* __restrict__ x,
                                                          const typename P::elem* __restrict__ w,
-                                                         typename P::elem* __restrict__ y, int64_t T_) {
+                                                         typename P::elem* __restrict__ y, int64_t T_,
+                                                         int acc) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaFwdSmem<P>;
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
     p2_last_inv<P>(rh, nv);
     p2_dc_inv<P>(rh, nv);
     __syncthreads();
-    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv);
+    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv, acc != 0);
     __syncthreads();
   }
 }
@@ -602,13 +603,13 @@ bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const
 
 template <typename P, int Q>
 bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
-                     cudaStream_t st) {
+                     cudaStream_t st, int acc) {
   using L = BcaFwdSmem<P>;
   auto k = bca_fwd2_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_, acc);
   return true;
 }
 

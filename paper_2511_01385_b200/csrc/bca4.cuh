@@ -32,7 +32,8 @@ struct BcaFwd4Smem {  // [H x PIPES][W][TWf][TWi]
 template <typename P, int Q, int PIPES>
 __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd4_kernel(const typename P::elem* __restrict__ x,
                                                                    const typename P::elem* __restrict__ w,
-                                                                   typename P::elem* __restrict__ y, int64_t T_) {
+                                                                   typename P::elem* __restrict__ y, int64_t T_,
+                                                                   int acc) {
   constexpr int q = Q;
   using L = BcaFwd4Smem<P, PIPES>;
   constexpr int N = P::N, NT = P::NT;
@@ -78,20 +79,20 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd4_kernel(const typena
     p2_last_inv<P>(rh, nv);
     p2_dc_inv<P>(rh, nv);
     named_bar(bid, NT);
-    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv);
+    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv, acc != 0);
     named_bar(bid, NT);
   }
 }
 
 template <typename P, int Q, int PIPES>
 bool launch_bca_fwd4(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
-                     cudaStream_t st) {
+                     cudaStream_t st, int acc) {
   using L = BcaFwd4Smem<P, PIPES>;
   auto k = bca_fwd4_kernel<P, Q, PIPES>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, PIPES * P::NT, L::BYTES, ((T_ + TT - 1) / TT + PIPES - 1) / PIPES, sms);
   if (grid <= 0) return false;
-  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_);
+  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_, acc);
   return true;
 }
 

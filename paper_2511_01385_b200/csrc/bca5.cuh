@@ -54,7 +54,8 @@ struct BcaFwd5Smem {  // [stage x PIPES][H x PIPES][TWf][TWi][bars x PIPES][tmem
 template <typename P, int Q, int PIPES>
 __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typename P::elem* __restrict__ x,
                                                                    const typename P::elem* __restrict__ w,
-                                                                   typename P::elem* __restrict__ y, int64_t T_) {
+                                                                   typename P::elem* __restrict__ y, int64_t T_,
+                                                                   int acc) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaFwd5Smem<P, PIPES>;
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
     p2_last_inv<P>(rh, nv);
     p2_dc_inv<P>(rh, nv);
     named_bar(bid, NT);
-    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv);
+    p2_pass1_inv<P>(rh, y + tile * TT * tok_elems, nv, acc != 0);
     named_bar(bid, NT);
   }
   tmem_fence_before();
@@ -204,13 +205,13 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
 
 template <typename P, int Q, int PIPES>
 bool launch_bca_fwd5(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
-                     cudaStream_t st) {
+                     cudaStream_t st, int acc) {
   using L = BcaFwd5Smem<P, PIPES>;
   auto k = bca_fwd5_kernel<P, Q, PIPES>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, PIPES * P::NT, L::BYTES, ((T_ + TT - 1) / TT + PIPES - 1) / PIPES, sms);
   if (grid <= 0) return false;
-  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_);
+  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_, acc);
   return true;
 }
 
@@ -242,31 +243,32 @@ inline bool use_fwd4() {
 #endif
 // Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
 template <typename T, int Q>
-bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st) {
+bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st, int acc) {
   switch (p) {
     case 256:
       if constexpr (sizeof(T) == 2)
-        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 256, 16, 16>, Q, 2>(x, w, y, T_, sms, st);
-      return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st);
+        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 256, 16, 16>, Q, 2>(x, w, y, T_, sms, st, acc);
+      return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc);
     case 1024:
       if constexpr (sizeof(T) == 2) {
-        if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st);
-        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st);
+        if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc);
+        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc);
       }
       return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
-          x, w, y, T_, sms, st);
+          x, w, y, T_, sms, st, acc);
     default: return false;
   }
 }
 template <typename T>
-bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st) {
+bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st,
+                  int acc) {
   if (q_in != q_out) return false;
   switch (q_in) {
-    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st);
-    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st);
-    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st);
-    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st);
+    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st, acc);
+    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st, acc);
+    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st, acc);
+    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st, acc);
     default: return false;
   }
 }

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_fwd_tiled_kernel(const T
                                                                          const T* __restrict__ w,
                                                                          T* __restrict__ y, int64_t T_, int q_in,
                                                                          int q_out, int p, int logp, int vt,
-                                                                         int grp) {
+                                                                         int grp, int yacc) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float2* tw = reinterpret_cast<float2*>(smem);
@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_fwd_tiled_kernel(const T
       __syncthreads();
       inv_stages_smem(Y, nv, p, logp, tw);
       for (int v = 0; v < nv; ++v)
-        store_rows<T>(y + (t0 + v) * d_out + (int64_t)i * p, Y + (size_t)v * p, p, p, logp, /*rev=*/true);
+        store_rows<T>(y + (t0 + v) * d_out + (int64_t)i * p, Y + (size_t)v * p, p, p, logp, /*rev=*/true,
+                      yacc != 0);
       __syncthreads();
     }
   }

@@ -63,7 +63,7 @@ __device__ __forceinline__ void bca_weight_spectra(const T* __restrict__ w, floa
 template <typename T>
 __global__ void __launch_bounds__(kBcaThreads) bca_fwd_v1_kernel(const T* __restrict__ x, const T* __restrict__ w,
                                                                    T* __restrict__ y, int64_t T_, int q_in,
-                                                                   int q_out, int p, int logp) {
+                                                                   int q_out, int p, int logp, int yacc) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float2* tw = reinterpret_cast<float2*>(smem);
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kBcaThreads) bca_fwd_v1_kernel(const T* __rest
     }
     __syncthreads();
     inv_stages_smem(Ys, q_out, p, logp, tw);
-    store_rows<T>(y + t * q_out * p, Ys, q_out * p, p, logp, /*rev=*/true);
+    store_rows<T>(y + t * q_out * p, Ys, q_out * p, p, logp, /*rev=*/true, yacc != 0);
     __syncthreads();
   }
 }

@@ -11,7 +11,8 @@ template <typename T>
 bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int sms, cudaStream_t st);
 // bca2.cuh: fused BCA fast paths (square layers, q <= 4, p in {256, 512, 1024}).
 template <typename T>
-bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st);
+bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st,
+                  int acc);  // acc != 0: y += BCA(x)
 template <typename T>
 bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
                   int sms, cudaStream_t st);

@@ -483,8 +483,10 @@ __device__ __forceinline__ void p2_dc_inv(const P2Roles<P>& r, int nv) {
 }
 
 // inverse pass 1: H windows -> real signals in global memory
+// acc: dst += result (the BCA forward's y += BCA(x) mode) instead of dst = result
 template <typename P>
-__device__ __forceinline__ void p2_pass1_inv(const P2Roles<P>& r, typename P::elem* dst_tile, int nv) {
+__device__ __forceinline__ void p2_pass1_inv(const P2Roles<P>& r, typename P::elem* dst_tile, int nv,
+                                             bool acc = false) {
   using T = typename P::elem;
   constexpr int R = P::R, S = P::S;
   if (r.act1 && r.v1 < nv) {
@@ -497,6 +499,14 @@ __device__ __forceinline__ void p2_pass1_inv(const P2Roles<P>& r, typename P::el
     });
     rfft_inv_reg<R>(b);
     T* dst = dst_tile + r.s1;
+    if (acc) {
+      const uint32_t k65536 = kTwo16;
+      ct::static_for<0, R>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const float2 o = gio<T>::ld2(dst + S * i, k65536);
+        b[rev_bits<P::LR>(i)] = make_float2(b[rev_bits<P::LR>(i)].x + o.x, b[rev_bits<P::LR>(i)].y + o.y);
+      });
+    }
     ct::static_for<0, R>([&](auto I) {
       constexpr int i = decltype(I)::value;
       gio<T>::st2(dst + S * i, b[rev_bits<P::LR>(i)]);

@@ -126,10 +126,10 @@ __device__ __forceinline__ void load_rows(const T* __restrict__ g, float* s, int
 }
 
 // Store `count` elements to global g from fp32 smem s, reading element i of
-// each row from its bit-reversed slot when `rev` is set.
+// each row from its bit-reversed slot when `rev` is set; acc: g += values instead of g = values.
 template <typename T>
 __device__ __forceinline__ void store_rows(T* __restrict__ g, const float* s, int count, int n, int logn,
-                                           bool rev) {
+                                           bool rev, bool acc = false) {
   constexpr int VEC = io<T>::kVec;
   const int nvec = ((reinterpret_cast<uintptr_t>(g) & 15) == 0) ? count / VEC : 0;
   uint4* g4 = reinterpret_cast<uint4*>(g);
@@ -141,11 +141,18 @@ __device__ __forceinline__ void store_rows(T* __restrict__ g, const float* s, in
       const int row = i >> logn, col = i & (n - 1);
       f[e] = s[(row << logn) + (rev ? bitrev(col, logn) : col)];
     }
+    if (acc) {
+      float o[VEC];
+      io<T>::unpack16(g4[q], o);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) f[e] += o[e];
+    }
     __stcs(g4 + q, io<T>::pack16(f));
   }
   for (int i = nvec * VEC + threadIdx.x; i < count; i += blockDim.x) {
     const int row = i >> logn, col = i & (n - 1);
-    io<T>::st(g + i, s[(row << logn) + (rev ? bitrev(col, logn) : col)]);
+    const float v = s[(row << logn) + (rev ? bitrev(col, logn) : col)];
+    io<T>::st(g + i, acc ? v + io<T>::ld(g + i) : v);
   }
 }
 

@@ -42,13 +42,15 @@ def _lib():
         lib.rdfft_packed_mul.argtypes = [vp, vp, i64, i64, i64, i32, vp]
         lib.rdfft_packed_conjmul.argtypes = [vp, vp, i64, i64, i64, i32, vp]
         lib.bca_fwd.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
+        lib.bca_fwd_accum.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_bwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_bwd_accum.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.rdfft_decode.argtypes = [vp, vp, i64, i64, i32, vp]
         lib.rdfft_encode.argtypes = [vp, vp, i64, i64, i32, vp]
         lib.rdfft_packed_conj.argtypes = [vp, i64, i64, i32, vp]
         lib.rdfft_packed_axpy.argtypes = [vp, vp, ctypes.c_float, i64, i64, i64, i32, vp]
-        for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
+        for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum",
+                  "bca_bwd",
                   "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
                   "rdfft_abi_version"):
             getattr(lib, f).restype = i32
@@ -59,7 +61,7 @@ def _lib():
     return _LIB
 
 
-EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd",
+EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum", "bca_bwd",
            "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
            "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
 
@@ -128,8 +130,10 @@ def rdfft_packed_conjmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     return _packed("rdfft_packed_conjmul", a, b)
 
 
-def bca_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None = None) -> torch.Tensor:
-    """y = BCA(x) for x [..., d_in], w [q_out, q_in, p]; y [..., q_out*p] (allocated if None)."""
+def bca_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
+    """y = BCA(x) for x [..., d_in], w [q_out, q_in, p]; y [..., q_out*p] (allocated if None).
+    accumulate=True (bca_fwd_accum): y <- y + BCA(x), the adapter added onto the frozen path's
+    output W0 x in the same pass."""
     _check(x, "x")
     _check(w, "w")
     q_out, q_in, p = w.shape
@@ -137,11 +141,13 @@ def bca_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None = None) -> 
     if x.shape[-1] != d_in:
         raise ValueError(f"x last dim {x.shape[-1]} != q_in*p = {d_in}")
     if y is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs the y to add into")
         y = torch.empty(x.shape[:-1] + (d_out,), dtype=x.dtype, device=x.device)
     _check(y, "y")
     if w.dtype != x.dtype or y.dtype != x.dtype:
         raise ValueError("x, w, y must share a dtype")
-    _call("bca_fwd", _ptr(x), _ptr(w), _ptr(y), x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
+    _call("bca_fwd_accum" if accumulate else "bca_fwd", _ptr(x), _ptr(w), _ptr(y), x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
     return y
 
 

@@ -27,7 +27,7 @@ def declared_functions():
 
 def test_header_declares_the_north_star_calls():
     names = declared_functions()
-    for f in ["rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_bwd"]:
+    for f in ["rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum", "bca_bwd"]:
         assert f in names
 
 

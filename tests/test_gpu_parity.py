@@ -388,6 +388,22 @@ def test_bca_fwd_bwd_match_oracle(q_out, q_in, p, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("q_out,q_in,p", [(4, 4, 1024), (3, 3, 256), (2, 2, 512), (2, 3, 128), (16, 16, 256)])
+def test_bca_fwd_accum(q_out, q_in, p, dtype):
+    """bca_fwd_accum: y <- y + BCA(x) on every forward kernel family (the fused
+    p = 1024 / 256 / 512 kernels, the resident-spectra kernel for non-square q, the tiled kernel
+    for q = 16), against y0 + the oracle's block-circulant product."""
+    T = 37
+    x, w, _ = synth.bca_inputs(T, q_in * p, q_out * p, p, seed=p + 7 * q_in, dtype=dtype)
+    y0 = synth.randn((T, q_out * p), seed=p + 5, dtype=dtype)
+    y = y0.cuda()
+    R.bca_fwd(x.cuda(), w.cuda(), y, accumulate=True)
+    torch.cuda.synchronize()
+    ref = f64(y0) + o.bca_fwd(f64(x), f64(w))
+    assert rel_l2_rows(f64(y), ref) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("q,p", [(3, 256), (16, 256)])
 def test_bca_bwd_dx_overwrites_g_in_place(dtype, q, p):
     T = 50
