@@ -37,6 +37,33 @@ def bca(x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     return BCAFunction.apply(x, w)
 
 
+class BCAAddFunction(torch.autograd.Function):
+    """y = base + BCA(x), written into base's buffer by `bca_fwd_accum` (the adapter added onto the
+    frozen path's output in the same pass).  grad wrt base is grad_output itself,
+    so dx gets its own buffer here (grad_output cannot be overwritten)."""
+
+    @staticmethod
+    def forward(ctx, base: torch.Tensor, x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        x = x.contiguous()
+        if not base.is_contiguous():
+            raise ValueError("base must be contiguous (it is updated in place)")
+        ctx.save_for_backward(x, w)
+        ctx.mark_dirty(base)
+        return R.bca_fwd(x, w, base, accumulate=True)
+
+    @staticmethod
+    def backward(ctx, g: torch.Tensor):
+        x, w = ctx.saved_tensors
+        g = g.contiguous()
+        dx, dw = R.bca_bwd(x, w, g)
+        return g, dx, (dw if w.dtype == torch.float32 else dw.to(w.dtype))
+
+
+def bca_add(base: torch.Tensor, x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    """base + BCA(x), in place on base (autograd-aware)."""
+    return BCAAddFunction.apply(base, x, w)
+
+
 class BlockCirculantAdapter(torch.nn.Module):
     """y = BCA(x) with weight [out/p, in/p, p] (first columns of the circulant blocks)."""
 
@@ -48,8 +75,10 @@ class BlockCirculantAdapter(torch.nn.Module):
         self.p = p
         self.weight = torch.nn.Parameter(torch.randn(d_out // p, d_in // p, p, dtype=dtype, device=device) * std)
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
-        return bca(x, self.weight)
+    def forward(self, x: torch.Tensor, base: torch.Tensor | None = None) -> torch.Tensor:
+        """BCA(x), or base + BCA(x) accumulated into base's buffer when the frozen path's output
+        is given (e.g. adapter(x, base=linear(x)))."""
+        return bca(x, self.weight) if base is None else bca_add(base, x, self.weight)
 
     def extra_repr(self) -> str:
         q_out, q_in, p = self.weight.shape

@@ -94,3 +94,25 @@ def test_single_layer_peak_memory(B_, D, p):
     granule = 512 * 5  # caching-allocator rounding per block
     assert extra <= allowed + granule, (extra, allowed)
     assert x.grad.data_ptr() != 0
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("bf16", 2e-2)])
+def test_adapter_on_frozen_path_grads(dtype, tol):
+    """adapter(x, base=W0 x): y = W0 x + BCA(x) through bca_fwd_accum; grads wrt x (both paths),
+    w and the frozen output match the oracle."""
+    T, q, p = 29, 2, 256
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=91, dtype=dtype)
+    w0 = synth.randn((q * p, q * p), seed=92, dtype="f32") * (q * p) ** -0.5
+    layer = B.BlockCirculantAdapter(q * p, q * p, p, dtype=x.dtype, device="cuda")
+    with torch.no_grad():
+        layer.weight.copy_(w.cuda())
+    xc = x.cuda().requires_grad_(True)
+    w0c = w0.to(x.dtype).cuda()
+    base = xc @ w0c.t()
+    y = layer(xc, base=base)
+    y.backward(g.cuda())
+    xo, wo, go, w0o = f64(x), f64(w), f64(g), f64(w0.to(x.dtype))
+    assert rel(f64(y), xo @ w0o.T + o.bca_fwd(xo, wo)) <= tol
+    dxo, dwo = o.bca_bwd(xo, wo, go)
+    assert rel(f64(xc.grad), dxo + go @ w0o) <= tol
+    assert rel(f64(layer.weight.grad), dwo) <= (1e-5 if dtype == "f32" else 2e-2)

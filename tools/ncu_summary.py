@@ -64,7 +64,9 @@ def family(name):
     if "rdfft2o_inv_kernel" in name:
         return "rdfft_inv"
     if "rdfft2_kernel" in name:
-        return "rdfft_inv" if re.search(r",\s*(?:true|\(bool\)1|1)>\s*\(", name) else "rdfft_fwd"
+        if re.search(r"<float,", name) and re.search(r",\s*(?:true|\(bool\)1|1)>\s*(?:\(|$)", name):
+            return "bca_bwd"  # the bench's only fp32 transform: bca_bwd's in-place dw finalize
+        return "rdfft_inv" if re.search(r",\s*(?:true|\(bool\)1|1)>\s*(?:\(|$)", name) else "rdfft_fwd"
     for k, f in [("bca_fwd", "bca_fwd"), ("bca_bwd", "bca_bwd"), ("packed_mul", "packed_mul"),
                  ("rdfft2_kernel", "rdfft"), ("rdfft_v1", "rdfft_v1")]:
         if k in name:
@@ -106,11 +108,28 @@ def main():
     if a.launches and os.path.exists(a.launches):
         tot, cnt = launches(a.launches)
         s = sum(tot.values())
+        # the bench's own kernels (input generation by torch runs before the timed region)
+        ours = sum(v for k, v in tot.items() if family(k) != "other")
         md.append("## launch list (ncu --metrics gpu__time_duration.sum, cold-cache, serialised)\n")
-        md.append("| kernel | launches | total us | share |\n|---|---|---|---|")
+        md.append("Shares: of every launch in the process, and of the step (this library's kernels only; the "
+                  "torch kernels generate the inputs before the timed region).\n")
+        md.append("| kernel | launches | total us | share (all) | share of step |\n|---|---|---|---|---|")
+        fam_ncu = collections.defaultdict(float)
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-            md.append(f"| `{k}` | {cnt[k]} | {v * 1e6:.1f} | {100 * v / s:.1f}% |")
+            fam = family(k)
+            step_share = f"{100 * v / ours:.1f}%" if fam != "other" and ours > 0 else "-"
+            if fam != "other":
+                fam_ncu[fam] += v
+            md.append(f"| `{k}` | {cnt[k]} | {v * 1e6:.1f} | {100 * v / s:.1f}% | {step_share} |")
         md.append("")
+        if a.bench and os.path.exists(a.bench) and ours > 0:
+            seg = b["segments_ms"]
+            tseg = sum(seg.values())
+            md.append("Share of the step per kernel: ncu launch list (cold, serialised) vs the bench's CUDA events\n")
+            md.append("| kernel | ncu share | CUDA-event share |\n|---|---|---|")
+            for fam in seg:
+                md.append(f"| {fam} | {100 * fam_ncu.get(fam, 0) / ours:.1f}% | {100 * seg[fam] / tseg:.1f}% |")
+            md.append("")
     md.append("## full captures (`ncu --set full`, one launch each)\n")
     md.append("| kernel | grid x block | regs | us | DRAM R+W MB | DRAM % | issue % | occupancy % | "
               "smem bank conflicts ld/st | local ld/st |\n|---|---|---|---|---|---|---|---|---|---|")
