@@ -50,7 +50,8 @@ struct PlanL {
   static constexpr int MINB = 512 / NT;  // CTAs per SM the 128-register budget allows
   static_assert(S / 2 == NW2 * 16 || NT == 512, "pass-2 sets per thread");
   static constexpr int TW2N = 32 * 16, TW3N = (M3 / 4) * K3;
-  static constexpr size_t TW2_OFF = (size_t)N * 4;
+  static constexpr int HPAD = 64;  // additive pad: 4 floats per n/16 slots (see phys)
+  static constexpr size_t TW2_OFF = (size_t)(N + HPAD) * 4;
   static constexpr size_t TW3_OFF = TW2_OFF + (size_t)TW2N * 8;
   static constexpr size_t BYTES1 = TW3_OFF + (size_t)TW3N * 8;
   // cluster pair (n = 2N): cross-stage twiddles W_{2N}^{128 a} (a < N / 256) and W_{2N}^b (b < 128)
@@ -59,11 +60,29 @@ struct PlanL {
   static constexpr size_t BYTES2 = TWC_OFF + (size_t)(TWCA + TWCB) * 8;
   static constexpr size_t BYTES = BYTES1;
   static_assert(M3 >= 8 && M3 <= 32 && LS >= 8, "plan L shape");
-  __host__ __device__ static constexpr int swz(int w) { return ((w >> (LS - 4)) ^ (((w >> 5) & 1) << 2)) & 7; }
-  // float index of packed slot s
-  __host__ __device__ static constexpr int phys(int s) {
-    return ((s >> 5) << 5) + ((((s >> 2) & 7) ^ swz(s >> 5)) << 2) + (s & 3);
-  }
+  static_assert(4 * NT == (N >> 4), "store/load phase chunk i sits in pad period i");
+  // Float index of packed slot s: plain slots plus 4 floats of pad per n/16 slots.  The pass-1
+  // float4 window stores of 8 consecutive lanes differ exactly in slot bits LN-4 .. LN-2 (the
+  // bit-reversed low bits of their subsequence index), so the pad puts them on 8 distinct 16-byte
+  // bank groups; and since the pad only changes at multiples of n/16 >= 512 slots, every pass-2/3
+  // access is a per-thread base plus a compile-time offset (OffP2 / OffP3), no runtime arithmetic.
+  __host__ __device__ static constexpr int pad(int s) { return 4 * (s >> (LN - 4)); }
+  __host__ __device__ static constexpr int phys(int s) { return s + pad(s); }
+};
+
+// Compile-time offsets of a closed set's two slots {be + j m0 + k, be + (j+1) m0 - k} relative to
+// per-thread bases pa = &H[phys(be) + k] and pb = &H[phys(be) - k] (valid for 1 <= k <= m0/2 and
+// be a multiple of the pad period or of m0 * M; see PlanL::phys).
+template <typename P>
+struct OffP3 {  // pass 3: be = 0, m0 = 1024, k < 512 (k = 512: the half set uses b() for both)
+  __host__ __device__ static constexpr int a(int j) { return 1024 * j + P::pad(1024 * j); }
+  __host__ __device__ static constexpr int b(int j) { return 1024 * (j + 1) + P::pad(1024 * (j + 1) - 1); }
+};
+template <typename P>
+struct OffP2 {  // pass 2: be = ww 1024, m0 = 32, k <= 16; in-block pad only when n/16 < 1024
+  __host__ __device__ static constexpr int rel(int x) { return (P::LN - 4 < 10) ? 4 * (x >> (P::LN - 4)) : 0; }
+  __host__ __device__ static constexpr int a(int j) { return 32 * j + rel(32 * j); }
+  __host__ __device__ static constexpr int b(int j) { return 32 * (j + 1) + rel(32 * j + 31); }
 };
 
 // pass-3 twiddle W_n^{k r} for compile-time r = 4 a + b
@@ -81,19 +100,29 @@ struct LTw3 {
   }
 };
 
-// One closed set of a pass: window base `be`, block size m0, k in 1 .. m0/2 (k == m0/2: the
-// zero-imaginary set), M blocks.  tw.template at<r>() = W_W^{k r} (forward) / conj (inverse).
-template <typename P, int M, bool kInv, typename TW>
-__device__ __forceinline__ void pl_set(float* H, int be, int m0, int k, const TW& tw) {
+// One closed set of a pass: M blocks of size m0, set k (1 <= k <= m0/2), slots pa[OFF::a(j)]
+// (= be + j m0 + k) and pb[OFF::b(j)] (= be + (j+1) m0 - k).  half (k == m0/2, the zero-imaginary
+// set): both are the same slot; kHalfB: read it through pb (the pass-3 half set, whose pad follows
+// b()).  tw.template at<r>() = W_W^{k r} (forward) / conj (inverse).
+template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, typename TW>
+__device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW& tw) {
   constexpr int LM = ilog2c<M>();
-  const int W = m0 * M;
-  const bool half = (2 * k == m0);
   float zr[M], zi[M];
+  auto A = [&](auto J) -> float& {
+    constexpr int j = decltype(J)::value;
+    if constexpr (kHalfB) return pb[OFF::b(j)];
+    else return pa[OFF::a(j)];
+  };
+  auto B = [&](auto J) -> float& {
+    constexpr int j = decltype(J)::value;
+    return pb[OFF::b(j)];
+  };
   if (!kInv) {
     ct::static_for<0, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
-      zr[j] = H[P::phys(be + j * m0 + k)];
-      zi[j] = half ? 0.f : H[P::phys(be + (j + 1) * m0 - k)];
+      zr[j] = A(J);
+      if constexpr (kHalfB) zi[j] = 0.f;
+      else zi[j] = half ? 0.f : B(J);
     });
     ct::static_for<1, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
@@ -103,31 +132,42 @@ __device__ __forceinline__ void pl_set(float* H, int be, int m0, int k, const TW
       zi[j] = fmaf(q, t.y, zi[j] * t.x);
     });
     cfft_dit<M>(zr, zi);
+    // slot be + q m0 + k <- (q < M/2 ? Re : -Im) Y[q];  be + (M - q) m0 - k (= B(M-1-q)) <- the other
     ct::static_for<0, M>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
-      if constexpr (q < M / 2) {
-        H[P::phys(be + q * m0 + k)] = zr[q];
-        H[P::phys(be + W - q * m0 - k)] = zi[q];
-      } else {
+      if constexpr (q < M / 2) {  // (half set: B(M-1-q) is another slot of the same set)
+        A(Q) = zr[q];
+        B(ct::ic<M - 1 - q>{}) = zi[q];
+      } else if constexpr (!kHalfB) {
         if (!half) {
-          H[P::phys(be + q * m0 + k)] = -zi[q];
-          H[P::phys(be + W - q * m0 - k)] = zr[q];
+          A(Q) = -zi[q];
+          B(ct::ic<M - 1 - q>{}) = zr[q];
         }
       }
     });
   } else {
-    // Y[q] into register rev(q): q < M/2: Re at q m0 + k, Im at W - q m0 - k;
-    // q >= M/2: Re at W - q m0 - k, Im = -(value at q m0 + k)
+    // Y[q] into register rev(q): q < M/2: Re at A(q), Im at B(M-1-q); q >= M/2: Re at B(M-1-q),
+    // Im = -(value at A(q)).  Half set: A(q) = B(q) real for q < M/2 (mirror of the forward).
     ct::static_for<0, M>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
       constexpr int rq = rev_bits<LM>(q);
-      const float a = H[P::phys(be + q * m0 + k)], b = H[P::phys(be + W - q * m0 - k)];
-      if constexpr (q < M / 2) {
-        zr[rq] = a;
-        zi[rq] = b;
+      if constexpr (kHalfB) {
+        if constexpr (q < M / 2) {
+          zr[rq] = A(Q);
+          zi[rq] = B(ct::ic<M - 1 - q>{});
+        } else {
+          zr[rq] = B(ct::ic<M - 1 - q>{});
+          zi[rq] = -A(Q);
+        }
       } else {
-        zr[rq] = b;
-        zi[rq] = -a;
+        const float av = A(Q), bv = B(ct::ic<M - 1 - q>{});
+        if constexpr (q < M / 2) {
+          zr[rq] = av;
+          zi[rq] = bv;
+        } else {
+          zr[rq] = bv;
+          zi[rq] = -av;
+        }
       }
     });
     cfft_dit<M, true>(zr, zi);
@@ -142,19 +182,21 @@ __device__ __forceinline__ void pl_set(float* H, int be, int m0, int k, const TW
     ct::static_for<0, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
       constexpr int rj = rev_bits<LM>(j);
-      H[P::phys(be + j * m0 + k)] = zr[rj];
-      if (!half) H[P::phys(be + (j + 1) * m0 - k)] = zi[rj];
+      A(J) = zr[rj];
+      if constexpr (!kHalfB) {
+        if (!half) B(J) = zi[rj];
+      }
     });
   }
 }
 
-// DC set: slots be + j m0 (j < M) — the packed real M-point FFT (inverse: unscaled x scale).
-template <typename P, int M, bool kInv>
-__device__ __forceinline__ void pl_dc(float* H, int be, int m0, float scale) {
+// DC set: slots p0[OFF::a(j)] (j < M) — the packed real M-point FFT (inverse: unscaled x scale).
+template <typename P, int M, bool kInv, typename OFF>
+__device__ __forceinline__ void pl_dc(float* p0, float scale) {
   float d[M];
   ct::static_for<0, M>([&](auto J) {
     constexpr int j = decltype(J)::value;
-    d[j] = H[P::phys(be + j * m0)];
+    d[j] = p0[OFF::a(j)];
   });
   if (!kInv)
     rfft_fwd_reg<M>(d);
@@ -162,7 +204,7 @@ __device__ __forceinline__ void pl_dc(float* H, int be, int m0, float scale) {
     rfft_inv_reg<M>(d);
   ct::static_for<0, M>([&](auto J) {
     constexpr int j = decltype(J)::value;
-    H[P::phys(be + j * m0)] = d[j] * scale;
+    p0[OFF::a(j)] = d[j] * scale;
   });
 }
 
@@ -316,9 +358,13 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
     constexpr bool kI = decltype(inv)::value;
 #pragma unroll 1
     for (int i = 0; i < P::K3PT; ++i) {
-      const int kk = tid + NT * i, k3 = kk == 0 ? K3 : kk;
-      pl_set<P, M3, kI>(H, 0, 1024, k3, tw3_for(k3));
-      if (kk == 0) pl_dc<P, M3, kI>(H, 0, 1024, kI ? 1.0f / N : 1.0f);
+      const int kk = tid + NT * i;
+      if (kk == 0) {  // the zero-imaginary set k = 512 and the DC set
+        pl_set<P, M3, kI, OffP3<P>, true>(H + K3, H - K3, true, tw3_for(K3));
+        pl_dc<P, M3, kI, OffP3<P>>(H, kI ? 1.0f / N : 1.0f);
+      } else {
+        pl_set<P, M3, kI, OffP3<P>>(H + kk, H - kk, false, tw3_for(kk));
+      }
     }
   };
   // pass-2 lane: window ww, k2 = 1 .. 15; lane 0 of each window: k2 = 16 (zero imaginary) + DC
@@ -326,6 +372,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   const bool act2 = tid < P::NW2 * 16;
   LTw2 tw2;
   tw2.h = TW2 + (k2 - 1);
+  float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
   const uint32_t k65536 = kTwo16;
   __syncthreads();
   if constexpr (NC == 2) cooperative_groups::this_cluster().sync();  // peer's H mapped and live
@@ -346,23 +393,26 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         });
         rfft_fwd_reg<R>(b);
         const int w0 = rev_bits<P::LS>(2 * c), w1 = w0 + S / 2;
+        float* h0 = H + P::phys(w0 * 32);  // a window never crosses a pad boundary
+        float* h1 = H + P::phys(w1 * 32);
         ct::static_for<0, R / 4>([&](auto I) {
           constexpr int i = 4 * decltype(I)::value;
-          *reinterpret_cast<float4*>(H + P::phys(w0 * 32 + i)) = make_float4(b[i].x, b[i + 1].x, b[i + 2].x, b[i + 3].x);
-          *reinterpret_cast<float4*>(H + P::phys(w1 * 32 + i)) = make_float4(b[i].y, b[i + 1].y, b[i + 2].y, b[i + 3].y);
+          *reinterpret_cast<float4*>(h0 + i) = make_float4(b[i].x, b[i + 1].x, b[i + 2].x, b[i + 3].x);
+          *reinterpret_cast<float4*>(h1 + i) = make_float4(b[i].y, b[i + 1].y, b[i + 2].y, b[i + 3].y);
         });
       }
       __syncthreads();
-      if (act2) pl_set<P, 32, false>(H, ww * 1024, 32, k2, tw2);
-      if (act2 && k2 == 16) pl_dc<P, 32, false>(H, ww * 1024, 32, 1.0f);
+      if (act2) pl_set<P, 32, false, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
+      if (act2 && k2 == 16) pl_dc<P, 32, false, OffP2<P>>(h2, 1.0f);
       __syncthreads();
       pass3(std::false_type{});
       if constexpr (NC == 1) {
         __syncthreads();
-        for (int e = tid; e < N / 4; e += NT) {
-          const float4 f = *reinterpret_cast<const float4*>(H + P::phys(4 * e));
-          gio4<T>::st(xv + 4 * e, f);
-        }
+        ct::static_for<0, N / 4 / NT>([&](auto I) {  // chunk e = tid + NT i: phys(4 e) = 4 tid + (4 NT + 4) i
+          constexpr int i = decltype(I)::value;
+          const float4 f = *reinterpret_cast<const float4*>(H + 4 * tid + (4 * NT + 4) * i);
+          gio4<T>::st(xv + 4 * (tid + NT * i), f);
+        });
         __syncthreads();
       } else {
         cooperative_groups::this_cluster().sync();  // both windows complete and visible
@@ -371,8 +421,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       }
     } else {
       if constexpr (NC == 1) {
-        for (int e = tid; e < N / 4; e += NT)
-          *reinterpret_cast<float4*>(H + P::phys(4 * e)) = gio4<T>::ld(xv + 4 * e);
+        ct::static_for<0, N / 4 / NT>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          *reinterpret_cast<float4*>(H + 4 * tid + (4 * NT + 4) * i) = gio4<T>::ld(xv + 4 * (tid + NT * i));
+        });
         __syncthreads();
       } else {
         pl_cross_inv<P>(H0, H1, TWCa, twb, xv, r, tid, k65536);
@@ -380,17 +432,19 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       }
       pass3(std::true_type{});
       __syncthreads();
-      if (act2) pl_set<P, 32, true>(H, ww * 1024, 32, k2, tw2);
-      if (act2 && k2 == 16) pl_dc<P, 32, true>(H, ww * 1024, 32, 1.0f);
+      if (act2) pl_set<P, 32, true, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
+      if (act2 && k2 == 16) pl_dc<P, 32, true, OffP2<P>>(h2, 1.0f);
       __syncthreads();
       if (tid < S / 2) {  // inverse pass 1
         const int c = tid;
         const int w0 = rev_bits<P::LS>(2 * c), w1 = w0 + S / 2;
+        const float* h0 = H + P::phys(w0 * 32);
+        const float* h1 = H + P::phys(w1 * 32);
         float2 b[R];
         ct::static_for<0, R / 4>([&](auto I) {
           constexpr int i = 4 * decltype(I)::value;
-          const float4 f0 = *reinterpret_cast<const float4*>(H + P::phys(w0 * 32 + i));
-          const float4 f1 = *reinterpret_cast<const float4*>(H + P::phys(w1 * 32 + i));
+          const float4 f0 = *reinterpret_cast<const float4*>(h0 + i);
+          const float4 f1 = *reinterpret_cast<const float4*>(h1 + i);
           b[i] = make_float2(f0.x, f1.x);
           b[i + 1] = make_float2(f0.y, f1.y);
           b[i + 2] = make_float2(f0.z, f1.z);
