@@ -61,6 +61,7 @@ struct PlanL {
   static constexpr size_t BYTES = BYTES1;
   static_assert(M3 >= 8 && M3 <= 32 && LS >= 8, "plan L shape");
   static_assert(4 * NT == (N >> 4), "store/load phase chunk i sits in pad period i");
+  static_assert(NW2 % (2 * (N / 4096)) == 0, "pass-2 half-warp block pairing");
   // Float index of packed slot s: plain slots plus 4 floats of pad per n/16 slots.  The pass-1
   // float4 window stores of 8 consecutive lanes differ exactly in slot bits LN-4 .. LN-2 (the
   // bit-reversed low bits of their subsequence index), so the pad puts them on 8 distinct 16-byte
@@ -368,7 +369,12 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
     }
   };
   // pass-2 lane: window ww, k2 = 1 .. 15; lane 0 of each window: k2 = 16 (zero imaginary) + DC
-  const int ww = tid / 16, k2 = tid % 16 == 0 ? 16 : tid % 16;
+  // The two half-warps take blocks ww and ww + D, D = n/4096: their pads then differ by 16 floats
+  // (4 pad periods), so the half-warps' scalar accesses fall on complementary bank halves (with
+  // adjacent blocks they overlapped: 2-way conflicts on every pass-2 access).
+  constexpr int D2 = N / 4096;
+  const int w32 = tid / 32, hw = (tid / 16) & 1;
+  const int ww = (w32 % D2) + (w32 / D2) * 2 * D2 + hw * D2, k2 = tid % 16 == 0 ? 16 : tid % 16;
   const bool act2 = tid < P::NW2 * 16;
   LTw2 tw2;
   tw2.h = TW2 + (k2 - 1);
