@@ -27,10 +27,15 @@ namespace rdfft {
 
 constexpr int kBcaQMax = 4;
 
-template <typename P>
+// Resident weight-spectra rows: sized for q = kBcaQMax up to p = 1024 (unchanged layouts), for the
+// kernel's own q at p >= 2048 (a 4096-point spectrum row is ~17 KB).
+template <typename P, int Q>
+constexpr int bca_wrows() { return P::N >= 2048 ? Q * Q : kBcaQMax * kBcaQMax; }
+
+template <typename P, int Q = kBcaQMax>
 struct BcaFwdSmem {  // [stage x STAGES][H][W][TWf][TWi][bars]; STAGES = 0: pass 1 reads x from HBM
   static constexpr int STAGES = P::NSTG;
-  static constexpr int WF = kBcaQMax * kBcaQMax * P::ROWA + 16;
+  static constexpr int WF = bca_wrows<P, Q>() * P::ROWA + 16;
   static constexpr size_t H_OFF = (size_t)STAGES * P::STAGE;
   static constexpr size_t W_OFF = H_OFF + (size_t)P::HF * 8;
   static constexpr size_t TWF_OFF = W_OFF + (size_t)WF * 8;
@@ -145,8 +150,9 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
                                                          int acc) {
   constexpr int q = Q;
   using T = typename P::elem;
-  using L = BcaFwdSmem<P>;
+  using L = BcaFwdSmem<P, Q>;
   constexpr int N = P::N;
+  static_assert(Q * Q <= P::VT, "the weight prologue transforms q*q <= VT spectra in one pass");
   extern __shared__ float4 smem4[];
   unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
   float2* H = reinterpret_cast<float2*>(base + L::H_OFF);
@@ -439,9 +445,9 @@ int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
 // One thread group of NT = VT * LPV threads transforms the x tile and then the g tile (pass 1
 // straight from HBM, no staging), so the product and the dx inverse use every thread; a tile is
 // VT / q tokens.  Shared memory: Hx, Hg, W, tables.
-template <typename P>
+template <typename P, int Q = kBcaQMax>
 struct BcaBwd3Smem {
-  static constexpr int WF = kBcaQMax * kBcaQMax * P::ROWA + 16;
+  static constexpr int WF = bca_wrows<P, Q>() * P::ROWA + 16;
   static constexpr size_t HX_OFF = 0;
   static constexpr size_t HG_OFF = HX_OFF + (size_t)P::HF * 8;
   static constexpr size_t W_OFF = HG_OFF + (size_t)P::HF * 8;
@@ -457,7 +463,8 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
                                                             float* __restrict__ dw, int64_t T_) {
   constexpr int q = Q;
   using T = typename P::elem;
-  using L = BcaBwd3Smem<P>;
+  using L = BcaBwd3Smem<P, Q>;
+  static_assert(Q * Q <= P::VT, "the weight prologue transforms q*q <= VT spectra in one pass");
   constexpr int N = P::N, NT = P::NT, NI = N / 4;
   extern __shared__ float4 smem4[];
   unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
@@ -590,7 +597,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
 template <typename P, int Q>
 bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
                      typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
-  using L = BcaBwd3Smem<P>;
+  using L = BcaBwd3Smem<P, Q>;
   auto k = bca_bwd3_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
@@ -604,7 +611,7 @@ bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const
 template <typename P, int Q>
 bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
                      cudaStream_t st, int acc) {
-  using L = BcaFwdSmem<P>;
+  using L = BcaFwdSmem<P, Q>;
   auto k = bca_fwd2_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);

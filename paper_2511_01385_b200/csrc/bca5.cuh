@@ -250,6 +250,15 @@ bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cu
         if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 256, 16, 16>, Q, 2>(x, w, y, T_, sms, st, acc);
       return launch_bca_fwd2<Plan2<T, 256, 16, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc);
     case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc);
+    // p = 2048 / 4096 (the paper's p sweep at D = 4096): the 2-pass plan with 64-point
+    // register blocks (Plan2 R = 64), q * q <= VT weight spectra resident
+    case 2048:
+      if constexpr (Q <= 2) return launch_bca_fwd2<Plan2<T, 2048, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc);
+      return false;
+    case 4096:
+      if constexpr (Q == 1) return launch_bca_fwd2<Plan2<T, 4096, 64, 2, 1>, Q>(x, w, y, T_, sms, st, acc);
+      if constexpr (Q == 2) return launch_bca_fwd2<Plan2<T, 4096, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc);
+      return false;
     case 1024:
       if constexpr (sizeof(T) == 2) {
         if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc);

@@ -281,6 +281,12 @@ bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_
         if (use_bwd5()) return launch_bca_bwd5<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
       if (v4) return launch_bca_bwd4<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
       return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+    case 2048:  // see bca_fwd_fast_q
+      if constexpr (Q <= 2) return launch_bca_bwd3<Plan2<T, 2048, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st);
+      return false;
+    case 4096:
+      if constexpr (Q == 1) return launch_bca_bwd3<Plan2<T, 4096, 64, 2>, Q>(x, w, g, dx, dw, T_, sms, st);
+      return false;
     default: return false;
   }
 }

@@ -388,6 +388,29 @@ def test_bca_fwd_bwd_match_oracle(q_out, q_in, p, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("q,p", [(1, 2048), (2, 2048), (1, 4096), (2, 4096)])
+def test_bca_large_p_match_oracle(q, p, dtype):
+    """p = 2048 / 4096 (the paper's p sweep) on the fused kernels with 64-point
+    register blocks (forward, accumulate forward, backward with dx over g), against the oracle."""
+    T = 11
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=p + q, dtype=dtype)
+    xc, wc, gc = x.cuda(), w.cuda(), g.cuda()
+    y = R.bca_fwd(xc, wc)
+    y2 = synth.randn((T, q * p), seed=5, dtype=dtype).cuda()
+    y20 = f64(y2)
+    R.bca_fwd(xc, wc, y2, accumulate=True)
+    dx, dw = R.bca_bwd(xc, wc, gc, gc)  # dx overwrites g
+    torch.cuda.synchronize()
+    xo, wo, go = f64(x), f64(w), f64(g)
+    yo = o.bca_fwd(xo, wo)
+    assert rel_l2_rows(f64(y), yo) <= TOL[dtype]
+    assert rel_l2_rows(f64(y2), y20 + yo) <= TOL[dtype]
+    dxo, dwo = o.bca_bwd(xo, wo, go)
+    assert rel_l2_rows(f64(dx), dxo) <= TOL[dtype]
+    assert rel_l2_rows(f64(dw).reshape(1, -1), dwo.reshape(1, -1)) <= (1e-5 if dtype == "f32" else 2e-2)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("q_out,q_in,p", [(4, 4, 1024), (3, 3, 256), (2, 2, 512), (2, 3, 128), (16, 16, 256)])
 def test_bca_fwd_accum(q_out, q_in, p, dtype):
     """bca_fwd_accum: y <- y + BCA(x) on every forward kernel family (the fused
