@@ -285,7 +285,7 @@ bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_
       if constexpr (Q <= 2) return launch_bca_bwd3<Plan2<T, 2048, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st);
       return false;
     case 4096:
-      if constexpr (Q == 1) return launch_bca_bwd3<Plan2<T, 4096, 64, 2>, Q>(x, w, g, dx, dw, T_, sms, st);
+      if constexpr (Q == 1) return launch_bca_bwd3<Plan2<T, 4096, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st);
       return false;
     default: return false;
   }
