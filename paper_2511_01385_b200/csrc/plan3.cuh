@@ -568,8 +568,8 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
 #define RDFFT_FWD_NSTG 1  // forward staging depth for n = 512 / 1024 (0 = pass 1 straight from HBM)
 #endif
 // Returns true when a specialised kernel was launched for (n, T).
-// bf16 inverse, n = 512/1024: the staged-read kernel (plan2o.cuh; measured 64 -> 70-76 % of HBM);
-// everything else plan2 (the plan2o forward and n <= 256 measured slower).  RDFFT_PLAN2O=0 forces plan2.
+// bf16 inverse, n = 128..1024: the staged-read kernel (plan2o.cuh; measured 64 -> 70-76 % of HBM at
+// 512/1024); everything else plan2 (the plan2o forward measured slower).  RDFFT_PLAN2O=0 forces plan2.
 template <typename T, int N, int R, int VT>
 bool launch_p2(T* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
   if constexpr (sizeof(T) == 2 && N >= 512) {
@@ -578,6 +578,15 @@ bool launch_p2(T* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
       return !(e && *e == '0');
     }();
     if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, 1>>(x, batch, sms, st);
+  }
+  // bf16 n = 128 / 256: the staged-read inverse too (with the per-width staging skew it measured
+  // 0.47 -> 0.51 / 0.60 -> 0.68 of HBM; n = 256 with a 2-deep staging ring)
+  if constexpr (sizeof(T) == 2 && N >= 128 && N < 512) {
+    static const bool use_o = [] {
+      const char* e = std::getenv("RDFFT_PLAN2O");
+      return !(e && *e == '0');
+    }();
+    if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, (N == 256 ? 2 : 1)>>(x, batch, sms, st);
   }
   return launch_plan2<Plan2<T, N, R, VT, (N >= 512 ? RDFFT_FWD_NSTG : 2)>, Plan2<T, N, R, VT, (N >= 512 ? 1 : 2)>>(
       x, batch, inverse, sms, st);
