@@ -577,7 +577,8 @@ bool launch_p2(T* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
       const char* e = std::getenv("RDFFT_PLAN2O");
       return !(e && *e == '0');
     }();
-    if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, 1>>(x, batch, sms, st);
+    // n = 512: 2-deep TMA ring (0.71 -> 0.74 of HBM; at 1024 it costs a CTA per SM: 0.77 -> 0.75)
+    if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, (N == 512 ? 2 : 1)>>(x, batch, sms, st);
   }
   // bf16 n = 128 / 256: the staged-read inverse too (with the per-width staging skew it measured
   // 0.47 -> 0.51 / 0.60 -> 0.68 of HBM; n = 256 with a 2-deep staging ring)
