@@ -137,6 +137,15 @@ def cpu_threads():
 
 
 # --------------------------------------------------------------- reference arm
+def arm_config(batch: int, world: int) -> dict:
+    """The workload both arms report (the reference arm times the oracle on a sample of it)."""
+    T, d_in, p = BCA["T"], BCA["d_in"], BCA["p"]
+    return {"workload": f"rdFFT fwd+packed_mul+inv on 2^{batch.bit_length() - 1} x n={N_FFT} bf16 per GPU "
+                        f"+ BCA fwd+bwd LLaMA2-7B adapter (T={T}, d={d_in}, p={p}, bf16)",
+            "n": N_FFT, "batch_per_gpu": batch, "bca": BCA, "parallelism": f"dp{world}",
+            "l2": "inputs larger than L2 (2 GiB transform buffer per GPU between BCA fwd and bwd)"}
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -158,7 +167,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(1, args.steps),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"rdFFT fwd+inv n={N_FFT} bf16 batch 2^20 (sampled)"},
+            "data": "synthetic", "config": arm_config(args.batch, world),
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -321,10 +330,7 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"rdFFT fwd+packed_mul+inv on 2^{batch.bit_length() - 1} x n={n} bf16 per GPU "
-                                   f"+ BCA fwd+bwd LLaMA2-7B adapter (T={T}, d={d_in}, p={p}, bf16)",
-                       "n": n, "batch_per_gpu": batch, "bca": BCA, "parallelism": f"dp{world}",
-                       "l2": "inputs larger than L2 (2 GiB transform buffer per GPU between BCA fwd and bwd)"},
+            "config": arm_config(batch, world),
             "frac_of_hbm_peak": value / hbm, "hbm_peak_GBps": hbm,
             "transforms_per_s": world * 2 * batch / (fwdinv_ms * 1e-3),
             "bca_fwd_ms": seg["bca_fwd"], "bca_bwd_ms": seg["bca_bwd"],
