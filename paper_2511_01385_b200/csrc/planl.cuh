@@ -105,8 +105,14 @@ struct LTw3 {
 // (= be + j m0 + k) and pb[OFF::b(j)] (= be + (j+1) m0 - k).  half (k == m0/2, the zero-imaginary
 // set): both are the same slot; kHalfB: read it through pb (the pass-3 half set, whose pad follows
 // b()).  tw.template at<r>() = W_W^{k r} (forward) / conj (inverse).
-template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, typename TW>
-__device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW& tw) {
+// kG (pass 3 of the one-CTA plan): the forward stores its outputs straight to the global row and the
+// inverse reads its inputs straight from it — slot be + j m0 + k at ga[j m0], slot be + (j+1) m0 - k
+// at gb[(j+1) m0] (ga = row + k, gb = row - k) — instead of going through H and a chunked phase.
+template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false, typename TW>
+__device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW& tw,
+                                       typename P::elem* ga = nullptr, typename P::elem* gb = nullptr,
+                                       int m0 = 0, uint32_t k65536 = 0) {
+  using T = typename P::elem;
   constexpr int LM = ilog2c<M>();
   float zr[M], zi[M];
   auto A = [&](auto J) -> float& {
@@ -136,7 +142,17 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
     // slot be + q m0 + k <- (q < M/2 ? Re : -Im) Y[q];  be + (M - q) m0 - k (= B(M-1-q)) <- the other
     ct::static_for<0, M>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
-      if constexpr (q < M / 2) {  // (half set: B(M-1-q) is another slot of the same set)
+      if constexpr (kG) {
+        if constexpr (q < M / 2) {
+          gio<T>::st1(ga + q * m0, zr[q]);
+          gio<T>::st1(gb + (M - q) * m0, zi[q]);
+        } else if constexpr (!kHalfB) {
+          if (!half) {
+            gio<T>::st1(ga + q * m0, -zi[q]);
+            gio<T>::st1(gb + (M - q) * m0, zr[q]);
+          }
+        }
+      } else if constexpr (q < M / 2) {  // (half set: B(M-1-q) is another slot of the same set)
         A(Q) = zr[q];
         B(ct::ic<M - 1 - q>{}) = zi[q];
       } else if constexpr (!kHalfB) {
@@ -152,7 +168,16 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
     ct::static_for<0, M>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
       constexpr int rq = rev_bits<LM>(q);
-      if constexpr (kHalfB) {
+      if constexpr (kG) {
+        const float av = gio1<T>::ld(ga + q * m0, k65536), bv = gio1<T>::ld(gb + (M - q) * m0, k65536);
+        if constexpr (q < M / 2) {
+          zr[rq] = av;
+          zi[rq] = bv;
+        } else {
+          zr[rq] = bv;
+          zi[rq] = -av;
+        }
+      } else if constexpr (kHalfB) {
         if constexpr (q < M / 2) {
           zr[rq] = A(Q);
           zi[rq] = B(ct::ic<M - 1 - q>{});
@@ -189,6 +214,28 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
       }
     });
   }
+}
+
+// DC set of pass 3 with the global row on one side (kG): forward H -> row, inverse row -> H.
+template <typename P, int M, bool kInv, typename OFF>
+__device__ __forceinline__ void pl_dc_g(float* p0, typename P::elem* g0, int m0, float scale, uint32_t k65536) {
+  using T = typename P::elem;
+  float d[M];
+  ct::static_for<0, M>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    d[j] = kInv ? gio1<T>::ld(g0 + j * m0, k65536) : p0[OFF::a(j)];
+  });
+  if (!kInv)
+    rfft_fwd_reg<M>(d);
+  else
+    rfft_inv_reg<M>(d);
+  ct::static_for<0, M>([&](auto J) {
+    constexpr int j = decltype(J)::value;
+    if (!kInv)
+      gio<T>::st1(g0 + j * m0, d[j] * scale);
+    else
+      p0[OFF::a(j)] = d[j] * scale;
+  });
 }
 
 // DC set: slots p0[OFF::a(j)] (j < M) — the packed real M-point FFT (inverse: unscaled x scale).
@@ -355,16 +402,25 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
     t.w3 = make_float2(fmaf(t.w2.x, w.x, -t.w2.y * w.y), fmaf(t.w2.x, w.y, t.w2.y * w.x));
     return t;
   };
-  auto pass3 = [&](auto inv) {
+  // pass 3; one-CTA plan (NC = 1): the forward stores its outputs straight to the row xv and the
+  // inverse reads its inputs straight from it (no chunked H <-> HBM phase: two passes of shared
+  // traffic fewer per vector); the cluster pair keeps them in H for the cross stage.
+  constexpr bool kG3 = (NC == 1);
+  const uint32_t k65536 = kTwo16;
+  auto pass3 = [&](auto inv, T* xv) {
     constexpr bool kI = decltype(inv)::value;
 #pragma unroll 1
     for (int i = 0; i < P::K3PT; ++i) {
       const int kk = tid + NT * i;
       if (kk == 0) {  // the zero-imaginary set k = 512 and the DC set
-        pl_set<P, M3, kI, OffP3<P>, true>(H + K3, H - K3, true, tw3_for(K3));
-        pl_dc<P, M3, kI, OffP3<P>>(H, kI ? 1.0f / N : 1.0f);
+        pl_set<P, M3, kI, OffP3<P>, true, kG3>(H + K3, H - K3, true, tw3_for(K3), xv + K3, xv - K3, 1024, k65536);
+        if constexpr (kG3)
+          pl_dc_g<P, M3, kI, OffP3<P>>(H, xv, 1024, kI ? 1.0f / N : 1.0f, k65536);
+        else
+          pl_dc<P, M3, kI, OffP3<P>>(H, kI ? 1.0f / N : 1.0f);
       } else {
-        pl_set<P, M3, kI, OffP3<P>>(H + kk, H - kk, false, tw3_for(kk));
+        pl_set<P, M3, kI, OffP3<P>, false, kG3>(H + kk, H - kk, false, tw3_for(kk), xv + kk, xv - kk, 1024,
+                                                k65536);
       }
     }
   };
@@ -379,7 +435,6 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   LTw2 tw2;
   tw2.h = TW2 + (k2 - 1);
   float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
-  const uint32_t k65536 = kTwo16;
   __syncthreads();
   if constexpr (NC == 2) cooperative_groups::this_cluster().sync();  // peer's H mapped and live
   for (int64_t v = blockIdx.x / NC; v < batch; v += gridDim.x / NC) {
@@ -411,32 +466,20 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       if (act2) pl_set<P, 32, false, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
       if (act2 && k2 == 16) pl_dc<P, 32, false, OffP2<P>>(h2, 1.0f);
       __syncthreads();
-      pass3(std::false_type{});
+      pass3(std::false_type{}, xv);
       if constexpr (NC == 1) {
-        __syncthreads();
-        ct::static_for<0, N / 4 / NT>([&](auto I) {  // chunk e = tid + NT i: phys(4 e) = 4 tid + (4 NT + 4) i
-          constexpr int i = decltype(I)::value;
-          const float4 f = *reinterpret_cast<const float4*>(H + 4 * tid + (4 * NT + 4) * i);
-          gio4<T>::st(xv + 4 * (tid + NT * i), f);
-        });
-        __syncthreads();
+        __syncthreads();  // H is read by pass 3 until here; the next vector's pass 1 writes it
       } else {
         cooperative_groups::this_cluster().sync();  // both windows complete and visible
         pl_cross_fwd<P>(H0, H1, TWCa, twb, xv, r, tid);
         cooperative_groups::this_cluster().sync();  // the peer is done reading this H
       }
     } else {
-      if constexpr (NC == 1) {
-        ct::static_for<0, N / 4 / NT>([&](auto I) {
-          constexpr int i = decltype(I)::value;
-          *reinterpret_cast<float4*>(H + 4 * tid + (4 * NT + 4) * i) = gio4<T>::ld(xv + 4 * (tid + NT * i));
-        });
-        __syncthreads();
-      } else {
+      if constexpr (NC == 2) {
         pl_cross_inv<P>(H0, H1, TWCa, twb, xv, r, tid, k65536);
         cooperative_groups::this_cluster().sync();  // both windows written (half of each remotely)
       }
-      pass3(std::true_type{});
+      pass3(std::true_type{}, xv);  // NC = 1: reads the row straight from HBM
       __syncthreads();
       if (act2) pl_set<P, 32, true, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
       if (act2 && k2 == 16) pl_dc<P, 32, true, OffP2<P>>(h2, 1.0f);
