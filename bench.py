@@ -185,7 +185,10 @@ def run_gpu(args):
 
     world, rank, local = dist_env()
     if world > 1:
-        dist.init_process_group("nccl")
+        # NCCL over NVLink on the box; RDFFT_DIST_BACKEND=gloo lets the N > 1 logic run with several
+        # ranks on one GPU (a functional check of barriers / max-over-ranks / the dw all-reduce)
+        dist.init_process_group(os.environ.get("RDFFT_DIST_BACKEND", "nccl"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if rank == 0:
@@ -331,7 +334,7 @@ def run_gpu(args):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": arm_config(batch, world),
-            "frac_of_hbm_peak": value / hbm, "hbm_peak_GBps": hbm,
+            "frac_of_hbm_peak": value / (world * hbm), "hbm_peak_GBps": hbm,
             "transforms_per_s": world * 2 * batch / (fwdinv_ms * 1e-3),
             "bca_fwd_ms": seg["bca_fwd"], "bca_bwd_ms": seg["bca_bwd"],
             "bca_fwd_bwd_ms": seg["bca_fwd"] + seg["bca_bwd"],
