@@ -270,10 +270,10 @@ bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_
                     cudaStream_t st) {
   const bool v4 = use_bwd4() && Q % 2 == 0;  // odd q: half the pair-split product is predicated off
   switch (p) {
-    case 256:  // odd q predicates half of the pair-split product: the 2-group kernel measured faster
-      if (v4) return launch_bca_bwd4<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      return launch_bca_bwd2<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-    case 512:
+    case 256:  // the single-group kernel (all threads in every phase): RoBERTa-base bf16 bwd 0.073 -> 0.061 ms,
+               // RoBERTa-large 0.098 -> 0.081 ms (the 2-group / pair-split kernels measured slower here)
+      return launch_bca_bwd3<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+    case 512:  // (the single-group kernel measured slower here: 0.171 -> 0.200 ms at q = 4)
       if (v4) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
       return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st);
     case 1024:

@@ -15,6 +15,8 @@ from paper_2511_01385_b200 import rdfft as R  # noqa: E402
 SHAPES = {"roberta_base": (32 * 512, 768, 256), "roberta_large": (32 * 512, 1024, 256),
           "llama2_7b": (8 * 2048, 4096, 1024)}
 # the paper's single-layer sweep (Tab. 1 / Fig. 3 setting): D = 4096, p = 128 .. 4096
+SHAPES["d2048_p512"] = (8 * 2048, 2048, 512)   # q = 4 at p = 512
+SHAPES["d1536_p512"] = (8 * 2048, 1536, 512)   # q = 3
 for _p in (128, 256, 512, 2048, 4096):
     SHAPES[f"d4096_p{_p}"] = (8 * 2048, 4096, _p)
 
