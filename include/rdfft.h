@@ -128,6 +128,21 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
 int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
                   int64_t d_out, int64_t p, int dtype, void* stream);
 
+/* bca_fwd_spectral / bca_bwd_spectral — the layer with SPECTRAL-RESIDENT weights
+ * (the paper keeps c's spectrum between steps, and its
+ * training updates it in place: spectral-domain SGD with rdfft_packed_axpy):
+ *   W:  fp32 [q_out][q_in][p] packed spectra W_ij = rdFFT(w_ij) (e.g. rdfft_fwd
+ *       of an fp32 copy of w), read only; the kernels skip their weight transform.
+ *   bca_fwd_spectral:  y = IrdFFT(sum_j W_ij (.) X_j)  (accumulate != 0: y += ...)
+ *   bca_bwd_spectral:  dx as bca_bwd (dx may alias g iff d_in == d_out), and
+ *       dW = sum_t conj(X_tj) (.) G_ti as fp32 PACKED SPECTRA, no inverse — the
+ *       gradient with respect to W (accumulate != 0: added to dW's contents).
+ *   Other arguments, layouts and errors as bca_fwd / bca_bwd.                 */
+int bca_fwd_spectral(const void* x, const float* W, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
+                     int dtype, int accumulate, void* stream);
+int bca_bwd_spectral(const void* x, const float* W, const void* g, void* dx, float* dW, int64_t T, int64_t d_in,
+                     int64_t d_out, int64_t p, int dtype, int accumulate, void* stream);
+
 /* ---- packed-spectrum utilities ---------------------------
  * rdfft_decode — the explicit decode step of the paper's Limitations
  * ("explicit complex access needs a decode step that breaks the

@@ -159,7 +159,7 @@ int grid_for(K kernel, int threads, size_t smem, int64_t units) {
 
 
 int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, int q_out, int p, int logp, int dtype,
-                  cudaStream_t st, int acc) {
+                  cudaStream_t st, int acc, const float* wspec) {
   BcaTiledPlan plan{};
   if (!bca_tiled_plan(false, false, T, q_in, q_out, p, num_sms(), &plan)) return RDFFT_E_SHAPE;
   const dim3 grid((unsigned)std::min<int64_t>(plan.tiles, (int64_t)num_sms() * 4), (unsigned)plan.groups);
@@ -168,14 +168,14 @@ int bca_fwd_tiled(const void* x, const void* w, void* y, int64_t T, int q_in, in
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
     k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
                                                   static_cast<float*>(y), T, q_in, q_out, p, logp, plan.vt, plan.grp,
-                                                  acc);
+                                                  acc, wspec);
   } else {
     auto k = bca_fwd_tiled_kernel<__nv_bfloat16>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
     k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const __nv_bfloat16*>(x),
                                                   static_cast<const __nv_bfloat16*>(w),
                                                   static_cast<__nv_bfloat16*>(y), T, q_in, q_out, p, logp, plan.vt,
-                                                  plan.grp, acc);
+                                                  plan.grp, acc, wspec);
   }
   return launched();
 }
@@ -270,39 +270,43 @@ int rdfft_packed_conjmul(void* a, const void* b, int64_t batch, int64_t n, int64
   return packed(a, b, batch, n, b_batch, dtype, stream, true);
 }
 
+// wspec: the caller's resident weight spectra (fp32 packed, [q_out][q_in][p]) instead of w
 static int bca_fwd_impl(const void* x, const void* w, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
-                        int dtype, void* stream, int acc) {
+                        int dtype, void* stream, int acc, const float* wspec = nullptr) {
+  if (wspec) w = wspec;  // validated and alias-checked as the weight operand (fp32: see ws below)
   int rc = bca_check(x, w, T, d_in, d_out, p, dtype);
   if (rc != RDFFT_OK || T == 0) return rc;
   if (!y) return RDFFT_E_NULL;
   if (!aligned16(y)) return RDFFT_E_ALIGN;
   const size_t s = dsize(dtype);
   const int q_in = (int)(d_in / p), q_out = (int)(d_out / p);
-  if (overlap(y, T * d_out * s, x, T * d_in * s) || overlap(y, T * d_out * s, w, (size_t)q_out * q_in * p * s))
+  const size_t ws = wspec ? 4 : s;
+  if (overlap(y, T * d_out * s, x, T * d_in * s) || overlap(y, T * d_out * s, w, (size_t)q_out * q_in * p * ws))
     return RDFFT_E_ALIAS;
   const size_t smem = bca_fwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int logp = ilog2(p);
-  if (smem > 227 * 1024) return bca_fwd_tiled(x, w, y, T, q_in, q_out, (int)p, logp, dtype, st, acc);
+  if (smem > 227 * 1024) return bca_fwd_tiled(x, w, y, T, q_in, q_out, (int)p, logp, dtype, st, acc, wspec);
   const bool fast =
       dtype == RDFFT_F32
           ? bca_fwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w), static_cast<float*>(y), T,
-                                q_in, q_out, (int)p, num_sms(), st, acc)
+                                q_in, q_out, (int)p, num_sms(), st, acc, wspec)
           : bca_fwd_fast<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
-                                        static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, num_sms(), st, acc);
+                                        static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, num_sms(), st, acc,
+                                        wspec);
   if (fast) return launched();
   if (dtype == RDFFT_F32) {
     auto k = bca_fwd_v1_kernel<float>;
     const int grid = grid_for(k, kBcaThreads, smem, T);
     if (!grid) return RDFFT_E_SHAPE;
     k<<<grid, kBcaThreads, smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
-                                       static_cast<float*>(y), T, q_in, q_out, (int)p, logp, acc);
+                                       static_cast<float*>(y), T, q_in, q_out, (int)p, logp, acc, wspec);
   } else {
     auto k = bca_fwd_v1_kernel<__nv_bfloat16>;
     const int grid = grid_for(k, kBcaThreads, smem, T);
     if (!grid) return RDFFT_E_SHAPE;
     k<<<grid, kBcaThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
-                                       static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, logp, acc);
+                                       static_cast<__nv_bfloat16*>(y), T, q_in, q_out, (int)p, logp, acc, wspec);
   }
   return launched();
 }
@@ -317,8 +321,18 @@ int bca_fwd_accum(const void* x, const void* w, void* y, int64_t T, int64_t d_in
   return bca_fwd_impl(x, w, y, T, d_in, d_out, p, dtype, stream, 1);
 }
 
+int bca_fwd_spectral(const void* x, const float* W, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
+                     int dtype, int accumulate, void* stream) {
+  if (!W) return T == 0 ? RDFFT_OK : RDFFT_E_NULL;
+  return bca_fwd_impl(x, nullptr, y, T, d_in, d_out, p, dtype, stream, accumulate ? 1 : 0, W);
+}
+
+// wspec: resident weight spectra instead of w; spectral_dw: leave dw as accumulated packed spectra
+// (no finalize inverse) — the spectral-domain gradient of the resident spectra.
 static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
-                 int64_t d_out, int64_t p, int dtype, void* stream, bool accumulate) {
+                 int64_t d_out, int64_t p, int dtype, void* stream, bool accumulate, const float* wspec = nullptr,
+                 bool spectral_dw = false) {
+  if (wspec) w = wspec;
   int rc = bca_check(x, w, T, d_in, d_out, p, dtype);
   if (rc != RDFFT_OK) return rc;
   if (!dw) return RDFFT_E_NULL;
@@ -327,13 +341,14 @@ static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, f
   const int q_in = (int)(d_in / p), q_out = (int)(d_out / p);
   const size_t nw = (size_t)q_out * q_in * p;
   const size_t xb = T * d_in * s, gb = T * d_out * s;
+  const size_t ws = wspec ? 4 : s;
   if (T > 0) {
     if (!g || !dx) return RDFFT_E_NULL;
     if (!aligned16(g) || !aligned16(dx)) return RDFFT_E_ALIGN;
-    if (overlap(dx, xb, x, xb) || overlap(dx, xb, w, nw * s)) return RDFFT_E_ALIAS;
+    if (overlap(dx, xb, x, xb) || overlap(dx, xb, w, nw * ws)) return RDFFT_E_ALIAS;
     if (overlap(dx, xb, g, gb) && !(dx == g && d_in == d_out)) return RDFFT_E_ALIAS;
   }
-  if (overlap(dw, nw * 4, x, xb) || overlap(dw, nw * 4, w, nw * s) || overlap(dw, nw * 4, g, gb) ||
+  if (overlap(dw, nw * 4, x, xb) || overlap(dw, nw * 4, w, nw * ws) || overlap(dw, nw * 4, g, gb) ||
       overlap(dw, nw * 4, dx, xb))
     return RDFFT_E_ALIAS;
   const size_t smem = bca_bwd_smem_floats(q_in, q_out, (int)p) * sizeof(float);
@@ -341,7 +356,9 @@ static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, f
   BcaTiledPlan plan{};
   if (tiled && !bca_tiled_plan(true, dx == g, T, q_in, q_out, (int)p, num_sms(), &plan)) return RDFFT_E_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (accumulate) {  // old dw -> its spectra; the kernels add theirs; the finalize inverse returns old + new
+  if (accumulate && spectral_dw) {
+    // dW already holds spectra: the kernels add this call's on top
+  } else if (accumulate) {  // old dw -> its spectra; the kernels add theirs; the finalize inverse returns old + new
     if ((rc = launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/false, st)) != RDFFT_OK)
       return rc;
   } else if (cudaMemsetAsync(dw, 0, nw * sizeof(float), st) != cudaSuccess) {
@@ -355,27 +372,28 @@ static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, f
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
       k<<<grid, kBcaTiledThreads, plan.smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
                                                     static_cast<const float*>(g), static_cast<float*>(dx), dw, T,
-                                                    q_in, q_out, (int)p, logp, plan.vt, plan.grp);
+                                                    q_in, q_out, (int)p, logp, plan.vt, plan.grp, wspec);
     } else {
       auto k = bca_bwd_tiled_kernel<__nv_bfloat16>;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
       k<<<grid, kBcaTiledThreads, plan.smem, st>>>(
           static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
           static_cast<const __nv_bfloat16*>(g), static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out, (int)p, logp,
-          plan.vt, plan.grp);
+          plan.vt, plan.grp, wspec);
     }
     if ((rc = launched()) != RDFFT_OK) return rc;
+    if (spectral_dw) return RDFFT_OK;
     return launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/true, st);
   }
   const bool fast =
       !tiled && T > 0 && (dtype == RDFFT_F32
                     ? bca_bwd_fast<float>(static_cast<const float*>(x), static_cast<const float*>(w),
                                           static_cast<const float*>(g), static_cast<float*>(dx), dw, T, q_in, q_out,
-                                          (int)p, num_sms(), st)
+                                          (int)p, num_sms(), st, wspec)
                     : bca_bwd_fast<__nv_bfloat16>(
                           static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
                           static_cast<const __nv_bfloat16*>(g), static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out,
-                          (int)p, num_sms(), st));
+                          (int)p, num_sms(), st, wspec));
   if (fast) {
     if ((rc = launched()) != RDFFT_OK) return rc;
   } else if (T > 0 && !tiled) {
@@ -385,17 +403,18 @@ static int bca_bwd_impl(const void* x, const void* w, const void* g, void* dx, f
       if (!grid) return RDFFT_E_SHAPE;
       k<<<grid, kBcaThreads, smem, st>>>(static_cast<const float*>(x), static_cast<const float*>(w),
                                          static_cast<const float*>(g), static_cast<float*>(dx), dw, T, q_in, q_out,
-                                         (int)p, logp);
+                                         (int)p, logp, wspec);
     } else {
       auto k = bca_bwd_v1_kernel<__nv_bfloat16>;
       const int grid = grid_for(k, kBcaThreads, smem, T);
       if (!grid) return RDFFT_E_SHAPE;
       k<<<grid, kBcaThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x),
                                          static_cast<const __nv_bfloat16*>(w), static_cast<const __nv_bfloat16*>(g),
-                                         static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out, (int)p, logp);
+                                         static_cast<__nv_bfloat16*>(dx), dw, T, q_in, q_out, (int)p, logp, wspec);
     }
     if ((rc = launched()) != RDFFT_OK) return rc;
   }
+  if (spectral_dw) return RDFFT_OK;
   // dw finalise: in-place inverse rdFFT of the q_out*q_in accumulated fp32 spectra.
   return launch_transform<float>(dw, (int64_t)q_out * q_in, (int)p, /*inverse=*/true, st);
 }
@@ -408,6 +427,12 @@ int bca_bwd(const void* x, const void* w, const void* g, void* dx, float* dw, in
 int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* dw, int64_t T, int64_t d_in,
                   int64_t d_out, int64_t p, int dtype, void* stream) {
   return bca_bwd_impl(x, w, g, dx, dw, T, d_in, d_out, p, dtype, stream, true);
+}
+
+int bca_bwd_spectral(const void* x, const float* W, const void* g, void* dx, float* dW, int64_t T, int64_t d_in,
+                     int64_t d_out, int64_t p, int dtype, int accumulate, void* stream) {
+  if (!W) return RDFFT_E_NULL;
+  return bca_bwd_impl(x, nullptr, g, dx, dW, T, d_in, d_out, p, dtype, stream, accumulate != 0, W, true);
 }
 
 const char* rdfft_status_str(int status) {

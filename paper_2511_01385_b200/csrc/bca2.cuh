@@ -147,7 +147,7 @@ template <typename P, int Q>
 __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::elem* __restrict__ x,
                                                          const typename P::elem* __restrict__ w,
                                                          typename P::elem* __restrict__ y, int64_t T_,
-                                                         int acc) {
+                                                         int acc, const float* __restrict__ wspec) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaFwdSmem<P, Q>;
@@ -175,12 +175,15 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
   const P2Roles<P> rh(H, TWf, TWi, tid);
   auto tile_rows = [&](int64_t t) { return (int)((T_ - t * TT < TT ? T_ - t * TT : TT) * q); };
   __syncthreads();
-  // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors, into the resident region
-  if constexpr (L::STAGES > 0) {
-    if (tid == 0) stage_issue_rows<P>(w, q * q, base, bar);
-    mbar_wait(bar, 0);
-  }
-  {
+  // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors, into the resident region (or the caller's
+  // resident spectra copied in: wspec)
+  if (wspec) {
+    p2_load_spectra<P>(Wr, wspec, q * q, tid, P::NT);
+  } else {
+    if constexpr (L::STAGES > 0) {
+      if (tid == 0) stage_issue_rows<P>(w, q * q, base, bar);
+      mbar_wait(bar, 0);
+    }
     const P2Roles<P> rw(Wr, TWf, TWi, tid);
     if constexpr (L::STAGES > 0)
       p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(base), q * q, k65536);
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
     p2_dc_fwd<P>(rw, q * q);
   }
   __syncthreads();
-  uint32_t phase_use[2] = {1, 0};  // stage 0 has completed one phase (the weights)
+  uint32_t phase_use[2] = {wspec ? 0u : 1u, 0};  // stage 0 has completed one phase (the weights)
   if (tid == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
       const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
@@ -248,7 +251,8 @@ template <typename P, int Q>
 __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::elem* __restrict__ x,
                                                              const typename P::elem* __restrict__ w,
                                                              const typename P::elem* g, typename P::elem* dx,
-                                                             float* __restrict__ dw, int64_t T_) {
+                                                             float* __restrict__ dw, int64_t T_,
+                                                             const float* __restrict__ wspec) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaBwdSmem<P>;
@@ -288,9 +292,11 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
   const int nw = q * q;
   const int half = nw <= P::VT ? nw : 8;
   const int w0 = grp ? half : 0, wn = grp ? nw - half : half;
-  if (lt == 0 && wn > 0) stage_issue_rows<P>(w + (int64_t)w0 * N, wn, stg, gbar);
-  if (wn > 0) mbar_wait(gbar, 0);
-  {
+  if (wspec) {
+    p2_load_spectra<P>(Wr, wspec, nw, tid, NT2);
+  } else {
+    if (lt == 0 && wn > 0) stage_issue_rows<P>(w + (int64_t)w0 * N, wn, stg, gbar);
+    if (wn > 0) mbar_wait(gbar, 0);
     const P2Roles<P> rw(Wr + w0 * P::ROWA, TWf, TWi, lt);
     p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(stg), wn, k65536);
     __syncthreads();
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(2 * P::NT) bca_bwd2_kernel(const typename P::e
     p2_dc_fwd<P>(rw, wn);
   }
   __syncthreads();
-  uint32_t phase_use[2] = {wn > 0 ? 1u : 0u, 0};
+  uint32_t phase_use[2] = {(wn > 0 && !wspec) ? 1u : 0u, 0};
   if (lt == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
       const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
@@ -460,7 +466,8 @@ template <typename P, int Q>
 __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::elem* __restrict__ x,
                                                             const typename P::elem* __restrict__ w,
                                                             const typename P::elem* g, typename P::elem* dx,
-                                                            float* __restrict__ dw, int64_t T_) {
+                                                            float* __restrict__ dw, int64_t T_,
+                                                            const float* __restrict__ wspec) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaBwd3Smem<P, Q>;
@@ -484,7 +491,9 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
   const uint32_t k65536 = kTwo16;
   const P2Roles<P> rx(Hx, TWf, TWi, tid), rg(Hg, TWf, TWi, tid);
   __syncthreads();
-  {  // W_ij = rdFFT(w_ij): q*q <= VT vectors
+  if (wspec) {
+    p2_load_spectra<P>(Wr, wspec, q * q, tid, NT);
+  } else {  // W_ij = rdFFT(w_ij): q*q <= VT vectors
     const P2Roles<P> rw(Wr, TWf, TWi, tid);
     p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
     __syncthreads();
@@ -596,13 +605,14 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
 
 template <typename P, int Q>
 bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
-                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
+                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st,
+                     const float* wspec) {
   using L = BcaBwd3Smem<P, Q>;
   auto k = bca_bwd3_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, wspec);
   return true;
 }
 
@@ -610,25 +620,26 @@ bool launch_bca_bwd3(const typename P::elem* x, const typename P::elem* w, const
 
 template <typename P, int Q>
 bool launch_bca_fwd2(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
-                     cudaStream_t st, int acc) {
+                     cudaStream_t st, int acc, const float* wspec) {
   using L = BcaFwdSmem<P, Q>;
   auto k = bca_fwd2_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_, acc);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, w, y, T_, acc, wspec);
   return true;
 }
 
 template <typename P, int Q>
 bool launch_bca_bwd2(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
-                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
+                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st,
+                     const float* wspec) {
   using L = BcaBwdSmem<P>;
   auto k = bca_bwd2_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, 2 * P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_);
+  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, wspec);
   return true;
 }
 

@@ -33,7 +33,7 @@ template <typename P, int Q, int PIPES>
 __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd4_kernel(const typename P::elem* __restrict__ x,
                                                                    const typename P::elem* __restrict__ w,
                                                                    typename P::elem* __restrict__ y, int64_t T_,
-                                                                   int acc) {
+                                                                   int acc, const float* __restrict__ wspec) {
   constexpr int q = Q;
   using L = BcaFwd4Smem<P, PIPES>;
   constexpr int N = P::N, NT = P::NT;
@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd4_kernel(const typena
   const uint32_t k65536 = kTwo16;
   __syncthreads();
   // ---- prologue (pipe 0): W_ij = rdFFT(w_ij) into the resident region
-  if (pipe == 0) {
+  if (wspec) {
+    p2_load_spectra<P>(Wr, wspec, q * q, tid, PIPES * NT);
+  } else if (pipe == 0) {
     const P2Roles<P> rw(Wr, TWf, TWi, lt);
     p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
     named_bar(1, NT);
@@ -86,13 +88,13 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd4_kernel(const typena
 
 template <typename P, int Q, int PIPES>
 bool launch_bca_fwd4(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
-                     cudaStream_t st, int acc) {
+                     cudaStream_t st, int acc, const float* wspec) {
   using L = BcaFwd4Smem<P, PIPES>;
   auto k = bca_fwd4_kernel<P, Q, PIPES>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, PIPES * P::NT, L::BYTES, ((T_ + TT - 1) / TT + PIPES - 1) / PIPES, sms);
   if (grid <= 0) return false;
-  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_, acc);
+  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_, acc, wspec);
   return true;
 }
 

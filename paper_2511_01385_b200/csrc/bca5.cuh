@@ -55,7 +55,7 @@ template <typename P, int Q, int PIPES>
 __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typename P::elem* __restrict__ x,
                                                                    const typename P::elem* __restrict__ w,
                                                                    typename P::elem* __restrict__ y, int64_t T_,
-                                                                   int acc) {
+                                                                   int acc, const float* __restrict__ wspec) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaFwd5Smem<P, PIPES>;
@@ -106,12 +106,17 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
   // ---- prologue: W_ij = rdFFT(w_ij) into pipe 1's H (scratch), then into TMEM by pipe 0
   float2* Wtmp = Hbase + (size_t)(PIPES - 1) * P::HF;
   if (pipe == 0) {
-    const P2Roles<P> rw(Wtmp, TWf, TWi, lt);
-    p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
-    named_bar(1, NT);
-    p2_last_fwd<P>(rw, q * q);
-    p2_dc_fwd<P>(rw, q * q);
-    named_bar(1, NT);
+    if (wspec) {
+      p2_load_spectra<P>(Wtmp, wspec, q * q, lt, NT);
+      named_bar(1, NT);
+    } else {
+      const P2Roles<P> rw(Wtmp, TWf, TWi, lt);
+      p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
+      named_bar(1, NT);
+      p2_last_fwd<P>(rw, q * q);
+      p2_dc_fwd<P>(rw, q * q);
+      named_bar(1, NT);
+    }
     int oa, ob;
     bca_item_offsets<P>(u, oa, ob);
 #pragma unroll
@@ -205,13 +210,13 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
 
 template <typename P, int Q, int PIPES>
 bool launch_bca_fwd5(const typename P::elem* x, const typename P::elem* w, typename P::elem* y, int64_t T_, int sms,
-                     cudaStream_t st, int acc) {
+                     cudaStream_t st, int acc, const float* wspec) {
   using L = BcaFwd5Smem<P, PIPES>;
   auto k = bca_fwd5_kernel<P, Q, PIPES>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, PIPES * P::NT, L::BYTES, ((T_ + TT - 1) / TT + PIPES - 1) / PIPES, sms);
   if (grid <= 0) return false;
-  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_, acc);
+  k<<<grid, PIPES * P::NT, L::BYTES, st>>>(x, w, y, T_, acc, wspec);
   return true;
 }
 
@@ -243,40 +248,41 @@ inline bool use_fwd4() {
 #endif
 // Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
 template <typename T, int Q>
-bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st, int acc) {
+bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st, int acc,
+                    const float* wspec) {
   switch (p) {
     case 256:  // single pipe, 1-deep staging for both dtypes (bf16: the 2-pipe kernel measured
                // 0.038 -> 0.036 ms slower on RoBERTa-base, 0.048 -> 0.045 on RoBERTa-large)
-      return launch_bca_fwd2<Plan2<T, 256, 16, 16, 1>, Q>(x, w, y, T_, sms, st, acc);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc);
+      return launch_bca_fwd2<Plan2<T, 256, 16, 16, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
     // p = 2048 / 4096 (the paper's p sweep at D = 4096): the 2-pass plan with 64-point
     // register blocks (Plan2 R = 64), q * q <= VT weight spectra resident
     case 2048:
-      if constexpr (Q <= 2) return launch_bca_fwd2<Plan2<T, 2048, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc);
+      if constexpr (Q <= 2) return launch_bca_fwd2<Plan2<T, 2048, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
       return false;
     case 4096:
-      if constexpr (Q == 1) return launch_bca_fwd2<Plan2<T, 4096, 64, 2, 1>, Q>(x, w, y, T_, sms, st, acc);
-      if constexpr (Q == 2) return launch_bca_fwd2<Plan2<T, 4096, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc);
+      if constexpr (Q == 1) return launch_bca_fwd2<Plan2<T, 4096, 64, 2, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
+      if constexpr (Q == 2) return launch_bca_fwd2<Plan2<T, 4096, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
       return false;
     case 1024:
       if constexpr (sizeof(T) == 2) {
-        if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc);
-        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc);
+        if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc, wspec);
+        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc, wspec);
       }
       return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
-          x, w, y, T_, sms, st, acc);
+          x, w, y, T_, sms, st, acc, wspec);
     default: return false;
   }
 }
 template <typename T>
 bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st,
-                  int acc) {
+                  int acc, const float* wspec) {
   if (q_in != q_out) return false;
   switch (q_in) {
-    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st, acc);
-    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st, acc);
-    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st, acc);
-    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st, acc);
+    case 1: return bca_fwd_fast_q<T, 1>(x, w, y, T_, p, sms, st, acc, wspec);
+    case 2: return bca_fwd_fast_q<T, 2>(x, w, y, T_, p, sms, st, acc, wspec);
+    case 3: return bca_fwd_fast_q<T, 3>(x, w, y, T_, p, sms, st, acc, wspec);
+    case 4: return bca_fwd_fast_q<T, 4>(x, w, y, T_, p, sms, st, acc, wspec);
     default: return false;
   }
 }

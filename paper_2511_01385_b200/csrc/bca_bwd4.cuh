@@ -32,7 +32,8 @@ template <typename P, int Q>
 __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P::elem* __restrict__ x,
                                                                 const typename P::elem* __restrict__ w,
                                                                 const typename P::elem* g, typename P::elem* dx,
-                                                                float* __restrict__ dw, int64_t T_) {
+                                                                float* __restrict__ dw, int64_t T_,
+                                                                const float* __restrict__ wspec) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaBwd3Smem<P>;
@@ -59,7 +60,9 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
   p2_zero_pads<P>(Wr, q * q, tid, NT2);
   const uint32_t k65536 = kTwo16;
   __syncthreads();
-  if (grp == 0) {  // W_ij = rdFFT(w_ij), q*q <= VT vectors
+  if (wspec) {
+    p2_load_spectra<P>(Wr, wspec, q * q, tid, NT2);
+  } else if (grp == 0) {  // W_ij = rdFFT(w_ij), q*q <= VT vectors
     const P2Roles<P> rw(Wr, TWf, TWi, lt);
     p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
     named_bar(kBarG0, NT);
@@ -186,13 +189,14 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
 
 template <typename P, int Q>
 bool launch_bca_bwd4(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
-                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
+                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st,
+                     const float* wspec) {
   using L = BcaBwd3Smem<P>;
   auto k = bca_bwd4_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, 2 * P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_);
+  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, wspec);
   return true;
 }
 

@@ -30,7 +30,8 @@ template <typename P, int Q>
 __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P::elem* __restrict__ x,
                                                                 const typename P::elem* __restrict__ w,
                                                                 const typename P::elem* g, typename P::elem* dx,
-                                                                float* __restrict__ dw, int64_t T_) {
+                                                                float* __restrict__ dw, int64_t T_,
+                                                                const float* __restrict__ wspec) {
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaBwd5Smem<P>;
@@ -85,7 +86,9 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
   auto jrel = [&](int c, int r) { return 2 * c + (r ? 1 - h : h); };
   const uint32_t taddr = tmem + ((uint32_t)(32 * ((tid / 32) % 4)) << 16) + (uint32_t)(32 * (tid / 128));
   // ---- prologue: W = rdFFT(w) into Hg (scratch) by group 0, then every thread stores its 8 pairs
-  if (grp == 0) {
+  if (wspec) {
+    p2_load_spectra<P>(Hg, wspec, q * q, tid, NT2);
+  } else if (grp == 0) {
     const P2Roles<P> rw(Hg, TWf, TWi, lt);
     p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
     named_bar(kBarG0, NT);
@@ -235,13 +238,14 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
 
 template <typename P, int Q>
 bool launch_bca_bwd5(const typename P::elem* x, const typename P::elem* w, const typename P::elem* g,
-                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st) {
+                     typename P::elem* dx, float* dw, int64_t T_, int sms, cudaStream_t st,
+                     const float* wspec) {
   using L = BcaBwd5Smem<P>;
   auto k = bca_bwd5_kernel<P, Q>;
   constexpr int TT = P::VT / Q;
   const int grid = bca2_grid<P>(k, 2 * P::NT, L::BYTES, (T_ + TT - 1) / TT, sms);
   if (grid <= 0) return false;
-  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_);
+  k<<<grid, 2 * P::NT, L::BYTES, st>>>(x, w, g, dx, dw, T_, wspec);
   return true;
 }
 
@@ -267,25 +271,25 @@ inline bool use_bwd4() {
 
 template <typename T, int Q>
 bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
-                    cudaStream_t st) {
+                    cudaStream_t st, const float* wspec) {
   const bool v4 = use_bwd4() && Q % 2 == 0;  // odd q: half the pair-split product is predicated off
   switch (p) {
     case 256:  // the single-group kernel (all threads in every phase): RoBERTa-base bf16 bwd 0.073 -> 0.061 ms,
                // RoBERTa-large 0.098 -> 0.081 ms (the 2-group / pair-split kernels measured slower here)
-      return launch_bca_bwd3<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+      return launch_bca_bwd3<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
     case 512:  // (the single-group kernel measured slower here: 0.171 -> 0.200 ms at q = 4)
-      if (v4) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st);
+      if (v4) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
     case 1024:
       if constexpr (sizeof(T) == 2 && Q % 2 == 0)
-        if (use_bwd5()) return launch_bca_bwd5<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      if (v4) return launch_bca_bwd4<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
-      return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st);
+        if (use_bwd5()) return launch_bca_bwd5<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      if (v4) return launch_bca_bwd4<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
     case 2048:  // see bca_fwd_fast_q
-      if constexpr (Q <= 2) return launch_bca_bwd3<Plan2<T, 2048, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st);
+      if constexpr (Q <= 2) return launch_bca_bwd3<Plan2<T, 2048, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
       return false;
     case 4096:
-      if constexpr (Q == 1) return launch_bca_bwd3<Plan2<T, 4096, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st);
+      if constexpr (Q == 1) return launch_bca_bwd3<Plan2<T, 4096, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
       return false;
     default: return false;
   }
@@ -293,13 +297,13 @@ bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_
 
 template <typename T>
 bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
-                  int sms, cudaStream_t st) {
+                  int sms, cudaStream_t st, const float* wspec) {
   if (q_in != q_out) return false;
   switch (q_in) {
-    case 1: return bca_bwd_fast_q<T, 1>(x, w, g, dx, dw, T_, p, sms, st);
-    case 2: return bca_bwd_fast_q<T, 2>(x, w, g, dx, dw, T_, p, sms, st);
-    case 3: return bca_bwd_fast_q<T, 3>(x, w, g, dx, dw, T_, p, sms, st);
-    case 4: return bca_bwd_fast_q<T, 4>(x, w, g, dx, dw, T_, p, sms, st);
+    case 1: return bca_bwd_fast_q<T, 1>(x, w, g, dx, dw, T_, p, sms, st, wspec);
+    case 2: return bca_bwd_fast_q<T, 2>(x, w, g, dx, dw, T_, p, sms, st, wspec);
+    case 3: return bca_bwd_fast_q<T, 3>(x, w, g, dx, dw, T_, p, sms, st, wspec);
+    case 4: return bca_bwd_fast_q<T, 4>(x, w, g, dx, dw, T_, p, sms, st, wspec);
     default: return false;
   }
 }

@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_fwd_tiled_kernel(const T
                                                                          const T* __restrict__ w,
                                                                          T* __restrict__ y, int64_t T_, int q_in,
                                                                          int q_out, int p, int logp, int vt,
-                                                                         int grp, int yacc) {
+                                                                         int grp, int yacc,
+                                                                         const float* __restrict__ wspec) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float2* tw = reinterpret_cast<float2*>(smem);
@@ -54,9 +55,14 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_fwd_tiled_kernel(const T
     __syncthreads();
     fwd_stages_smem(X, nv * q_in, p, logp, tw);
     for (int i = i0; i < i1; ++i) {
-      load_rows<T>(w + (int64_t)i * d_in, Wr, q_in * p, p, logp, /*rev=*/true);
-      __syncthreads();
-      fwd_stages_smem(Wr, q_in, p, logp, tw);
+      if (wspec) {  // resident spectra: copy row block i
+        load_rows<float>(wspec + (int64_t)i * d_in, Wr, q_in * p, p, logp, /*rev=*/false);
+        __syncthreads();
+      } else {
+        load_rows<T>(w + (int64_t)i * d_in, Wr, q_in * p, p, logp, /*rev=*/true);
+        __syncthreads();
+        fwd_stages_smem(Wr, q_in, p, logp, tw);
+      }
       for (int it = threadIdx.x; it < nv * hb; it += blockDim.x) {
         const int v = it / hb;
         const PackedBin bin{p, it - v * hb};
@@ -87,7 +93,8 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_bwd_tiled_kernel(const T
                                                                          const T* __restrict__ w, const T* g, T* dx,
                                                                          float* __restrict__ dw, int64_t T_,
                                                                          int q_in, int q_out, int p, int logp,
-                                                                         int vt, int grp) {
+                                                                         int vt, int grp,
+                                                                         const float* __restrict__ wspec) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float2* tw = reinterpret_cast<float2*>(smem);
@@ -110,10 +117,16 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_bwd_tiled_kernel(const T
     __syncthreads();
     fwd_stages_smem(X, nv * ng, p, logp, tw);
     for (int i = 0; i < q_out; ++i) {
-      load_rows<T>(w + ((int64_t)i * q_in + j0) * p, WG, ng * p, p, logp, true);
+      if (wspec)
+        load_rows<float>(wspec + ((int64_t)i * q_in + j0) * p, WG, ng * p, p, logp, false);
+      else
+        load_rows<T>(w + ((int64_t)i * q_in + j0) * p, WG, ng * p, p, logp, true);
       for (int v = 0; v < nv; ++v) load_rows<T>(g + (t0 + v) * d_out + (int64_t)i * p, G + (size_t)v * p, p, p, logp, true);
       __syncthreads();
-      fwd_stages_smem(WG, ng + nv, p, logp, tw);
+      if (wspec)
+        fwd_stages_smem(G, nv, p, logp, tw);
+      else
+        fwd_stages_smem(WG, ng + nv, p, logp, tw);
       for (int it = threadIdx.x; it < ng * hb; it += blockDim.x) {
         const int j = it / hb;
         const PackedBin bin{p, it - j * hb};

@@ -54,7 +54,12 @@ __host__ __device__ constexpr size_t bca_bwd_smem_floats(int q_in, int q_out, in
 
 template <typename T>
 __device__ __forceinline__ void bca_weight_spectra(const T* __restrict__ w, float* Wsp, int nblk, int p,
-                                                   int logp, const float2* tw) {
+                                                   int logp, const float2* tw, const float* wspec) {
+  if (wspec) {  // resident spectra (packed, natural order): a plain copy
+    load_rows<float>(wspec, Wsp, nblk * p, p, logp, /*rev=*/false);
+    __syncthreads();
+    return;
+  }
   load_rows<T>(w, Wsp, nblk * p, p, logp, /*rev=*/true);
   __syncthreads();
   fwd_stages_smem(Wsp, nblk, p, logp, tw);
@@ -63,7 +68,8 @@ __device__ __forceinline__ void bca_weight_spectra(const T* __restrict__ w, floa
 template <typename T>
 __global__ void __launch_bounds__(kBcaThreads) bca_fwd_v1_kernel(const T* __restrict__ x, const T* __restrict__ w,
                                                                    T* __restrict__ y, int64_t T_, int q_in,
-                                                                   int q_out, int p, int logp, int yacc) {
+                                                                   int q_out, int p, int logp, int yacc,
+                                                                   const float* __restrict__ wspec) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float2* tw = reinterpret_cast<float2*>(smem);
@@ -72,7 +78,7 @@ __global__ void __launch_bounds__(kBcaThreads) bca_fwd_v1_kernel(const T* __rest
   float* Ys = Xs + (size_t)q_in * p;
   make_twiddles(tw, p);
   __syncthreads();
-  bca_weight_spectra<T>(w, Wsp, q_out * q_in, p, logp, tw);
+  bca_weight_spectra<T>(w, Wsp, q_out * q_in, p, logp, tw, wspec);
   const int hb = p >> 1;  // bins handled per block: k in [0, p/2)
   for (int64_t t = blockIdx.x; t < T_; t += gridDim.x) {
     load_rows<T>(x + t * q_in * p, Xs, q_in * p, p, logp, /*rev=*/true);
@@ -100,7 +106,7 @@ template <typename T>
 __global__ void __launch_bounds__(kBcaThreads) bca_bwd_v1_kernel(const T* __restrict__ x, const T* __restrict__ w,
                                                                    const T* g, T* dx, float* __restrict__ dw,
                                                                    int64_t T_, int q_in, int q_out, int p,
-                                                                   int logp) {
+                                                                   int logp, const float* __restrict__ wspec) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   float2* tw = reinterpret_cast<float2*>(smem);
@@ -113,7 +119,7 @@ __global__ void __launch_bounds__(kBcaThreads) bca_bwd_v1_kernel(const T* __rest
   make_twiddles(tw, p);
   for (size_t i = threadIdx.x; i < nW; i += blockDim.x) Acc[i] = 0.f;
   __syncthreads();
-  bca_weight_spectra<T>(w, Wsp, q_out * q_in, p, logp, tw);
+  bca_weight_spectra<T>(w, Wsp, q_out * q_in, p, logp, tw, wspec);
   const int hb = p >> 1;
   for (int64_t t = blockIdx.x; t < T_; t += gridDim.x) {
     load_rows<T>(x + t * q_in * p, XG, q_in * p, p, logp, /*rev=*/true);

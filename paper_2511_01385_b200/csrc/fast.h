@@ -12,10 +12,10 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
 // bca2.cuh: fused BCA fast paths (square layers, q <= 4, p in {256, 512, 1024}).
 template <typename T>
 bool bca_fwd_fast(const T* x, const T* w, T* y, int64_t T_, int q_in, int q_out, int p, int sms, cudaStream_t st,
-                  int acc);  // acc != 0: y += BCA(x)
+                  int acc, const float* wspec);  // acc != 0: y += BCA(x); wspec: resident W spectra (else w)
 template <typename T>
 bool bca_bwd_fast(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int q_in, int q_out, int p,
-                  int sms, cudaStream_t st);
+                  int sms, cudaStream_t st, const float* wspec);
 // utils.cu: packed-spectrum utilities
 template <typename T>
 void launch_packed_conj(T* a, int64_t batch, int n, int logn, int sms, cudaStream_t st);

@@ -409,6 +409,18 @@ __device__ __forceinline__ void p2_store(const P2Roles<P>& r, typename P::elem* 
   });
 }
 
+// Spectral-resident weights: nvec packed fp32 spectra (rows of n, e.g. rdfft_fwd
+// of w) copied into the half-pair layout the fused BCA kernels keep resident (dst rows row(v)).
+template <typename P>
+__device__ __forceinline__ void p2_load_spectra(float2* dst, const float* __restrict__ ws, int nvec, int lt,
+                                                int nthr) {
+  constexpr int N = P::N, HALF = N / 2;
+  for (int e = lt; e < nvec * HALF; e += nthr) {
+    const int v = e / HALF, hq = e % HALF;
+    dst[P::hidx(v, hq)] = make_float2(__ldg(ws + (int64_t)v * N + hq), __ldg(ws + (int64_t)v * N + hq + HALF));
+  }
+}
+
 // ---------------------------------------------------------------- inverse pieces
 // staged tile (natural order) -> H half pairs
 template <typename P>

@@ -43,6 +43,8 @@ def _lib():
         lib.rdfft_packed_conjmul.argtypes = [vp, vp, i64, i64, i64, i32, vp]
         lib.bca_fwd.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_fwd_accum.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, vp]
+        lib.bca_fwd_spectral.argtypes = [vp, vp, vp, i64, i64, i64, i64, i32, i32, vp]
+        lib.bca_bwd_spectral.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, i32, vp]
         lib.bca_bwd.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.bca_bwd_accum.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, i32, vp]
         lib.rdfft_decode.argtypes = [vp, vp, i64, i64, i32, vp]
@@ -50,6 +52,7 @@ def _lib():
         lib.rdfft_packed_conj.argtypes = [vp, i64, i64, i32, vp]
         lib.rdfft_packed_axpy.argtypes = [vp, vp, ctypes.c_float, i64, i64, i64, i32, vp]
         for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum",
+                  "bca_fwd_spectral", "bca_bwd_spectral",
                   "bca_bwd",
                   "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
                   "rdfft_abi_version"):
@@ -62,6 +65,7 @@ def _lib():
 
 
 EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum", "bca_bwd",
+           "bca_fwd_spectral", "bca_bwd_spectral",
            "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
            "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
 
@@ -174,6 +178,48 @@ def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor 
     _call("bca_bwd_accum" if accumulate else "bca_bwd", _ptr(x), _ptr(w), _ptr(g), _ptr(dx), _ptr(dw),
           x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
     return dx, dw
+
+
+def bca_fwd_spectral(x: torch.Tensor, W: torch.Tensor, y: torch.Tensor | None = None,
+                     accumulate: bool = False) -> torch.Tensor:
+    """y = BCA(x) from resident weight spectra W (fp32 [q_out, q_in, p], packed: rdfft_fwd of w)."""
+    _check(x, "x")
+    _check(W, "W")
+    if W.dtype != torch.float32:
+        raise ValueError("W (weight spectra) must be float32")
+    q_out, q_in, p = W.shape
+    d_in, d_out = q_in * p, q_out * p
+    if x.shape[-1] != d_in:
+        raise ValueError(f"x last dim {x.shape[-1]} != q_in*p = {d_in}")
+    if y is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs the y to add into")
+        y = torch.empty(x.shape[:-1] + (d_out,), dtype=x.dtype, device=x.device)
+    _check(y, "y")
+    _call("bca_fwd_spectral", _ptr(x), _ptr(W), _ptr(y), x.numel() // d_in, d_in, d_out, p, _dtype(x),
+          int(accumulate), _stream(x))
+    return y
+
+
+def bca_bwd_spectral(x: torch.Tensor, W: torch.Tensor, g: torch.Tensor, dx: torch.Tensor | None = None,
+                     dW: torch.Tensor | None = None, accumulate: bool = False):
+    """(dx, dW) with dW the fp32 packed-spectrum gradient of the resident spectra W (no inverse)."""
+    _check(x, "x")
+    _check(W, "W")
+    _check(g, "g")
+    q_out, q_in, p = W.shape
+    d_in, d_out = q_in * p, q_out * p
+    if dx is None:
+        dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
+    if dW is None:
+        if accumulate:
+            raise ValueError("accumulate=True needs the dW to add into")
+        dW = torch.empty((q_out, q_in, p), dtype=torch.float32, device=x.device)
+    _check(dx, "dx")
+    _check(dW, "dW")
+    _call("bca_bwd_spectral", _ptr(x), _ptr(W), _ptr(g), _ptr(dx), _ptr(dW), x.numel() // d_in, d_in, d_out, p,
+          _dtype(x), int(accumulate), _stream(x))
+    return dx, dW
 
 
 def rdfft_decode(p: torch.Tensor, c: torch.Tensor | None = None) -> torch.Tensor:

@@ -388,6 +388,41 @@ def test_bca_fwd_bwd_match_oracle(q_out, q_in, p, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("q_out,q_in,p", [(4, 4, 1024), (3, 3, 256), (4, 4, 256), (2, 2, 512), (3, 3, 512),
+                                          (1, 1, 2048), (1, 1, 4096), (2, 3, 128), (16, 16, 256)])
+def test_bca_spectral_weights(q_out, q_in, p, dtype):
+    """Spectral-resident weights: W = the oracle's packed spectra of w rounded to
+    fp32; forward (and accumulate) against the oracle's block-circulant product with the weights
+    those fp32 spectra represent (w_eff = oracle IrdFFT(W32)); backward dx against the oracle and
+    dW (left in the packed spectral domain) against the oracle's rdFFT of its dw.  Every kernel
+    family: fused p = 256 / 512 / 1024 / 4096, resident-spectra (2 x 3), tiled (q = 16)."""
+    T = 19
+    x, w, g = synth.bca_inputs(T, q_in * p, q_out * p, p, seed=p + 3 * q_in, dtype=dtype)
+    W32 = o.rdfft_fwd(f64(w).reshape(-1, p)).astype(np.float32).reshape(q_out, q_in, p)
+    w_eff = o.rdfft_inv(W32.astype(np.float64).reshape(-1, p)).reshape(q_out, q_in, p)
+    Wc = torch.from_numpy(W32).cuda()
+    xc, gc = x.cuda(), g.cuda()
+    y = R.bca_fwd_spectral(xc, Wc)
+    y2 = synth.randn((T, q_out * p), seed=9, dtype=dtype).cuda()
+    y20 = f64(y2)
+    R.bca_fwd_spectral(xc, Wc, y2, accumulate=True)
+    dx, dW = R.bca_bwd_spectral(xc, Wc, gc)
+    dW2 = dW.clone()
+    R.bca_bwd_spectral(xc, Wc, gc, dW=dW2, accumulate=True)
+    torch.cuda.synchronize()
+    xo, go = f64(x), f64(g)
+    yo = o.bca_fwd(xo, w_eff)
+    assert rel_l2_rows(f64(y), yo) <= TOL[dtype]
+    assert rel_l2_rows(f64(y2), y20 + yo) <= TOL[dtype]
+    dxo, dwo = o.bca_bwd(xo, w_eff, go)
+    assert rel_l2_rows(f64(dx), dxo) <= TOL[dtype]
+    dWo = o.rdfft_fwd(dwo.reshape(-1, p)).reshape(1, -1)
+    tol_w = 1e-5 if dtype == "f32" else 2e-2
+    assert rel_l2_rows(f64(dW).reshape(1, -1), dWo) <= tol_w
+    assert rel_l2_rows(f64(dW2).reshape(1, -1), 2 * dWo) <= tol_w
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("q,p", [(1, 2048), (2, 2048), (1, 4096), (2, 4096)])
 def test_bca_large_p_match_oracle(q, p, dtype):
     """p = 2048 / 4096 (the paper's p sweep) on the fused kernels with 64-point
