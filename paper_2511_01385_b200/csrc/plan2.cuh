@@ -141,7 +141,8 @@ struct Plan2 {
   // that width (capped at 64 B: two vectors per 128-byte wavefront or fewer).  n = 1024: 64 B (two
   // vectors per warp, complementary bank halves); bf16 n = 256 / 512: 32 B (four vectors per warp).
   static constexpr int SKEWB_ = (int)(P1 * (sizeof(T) == 2 ? 4 : 8));
-  static constexpr int SKEWB = SKEWB_ < 64 ? SKEWB_ : 64;
+  // (at least 16 B: the per-row TMA bulk copies need 16-byte aligned destinations)
+  static constexpr int SKEWB = SKEWB_ < 16 ? 16 : (SKEWB_ < 64 ? SKEWB_ : 64);
   static constexpr int SROW = N + SKEWB / (int)sizeof(T);
   static constexpr int STAGE = VT * SROW * (int)sizeof(T);
   static_assert(M <= 2 * R && M >= 4 && (R == 64 || R == 32 || R == 16), "2-pass plan shape");
