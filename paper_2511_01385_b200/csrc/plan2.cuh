@@ -145,6 +145,7 @@ struct Plan2 {
   static constexpr int SKEWB = SKEWB_ < 16 ? 16 : (SKEWB_ < 64 ? SKEWB_ : 64);
   static constexpr int SROW = N + SKEWB / (int)sizeof(T);
   static constexpr int STAGE = VT * SROW * (int)sizeof(T);
+  static_assert((SROW * (int)sizeof(T)) % 16 == 0, "staged rows must stay 16-byte aligned (TMA bulk copies)");
   static_assert(M <= 2 * R && M >= 4 && (R == 64 || R == 32 || R == 16), "2-pass plan shape");
   static_assert(NT % 32 == 0 && VT * P1 <= NT, "thread mapping");
   static_assert(VT <= 32, "one DC-set lane per vector in the last warp");
