@@ -254,7 +254,8 @@ bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cu
     case 256:  // single pipe, 1-deep staging for both dtypes (bf16: the 2-pipe kernel measured
                // 0.038 -> 0.036 ms slower on RoBERTa-base, 0.048 -> 0.045 on RoBERTa-large)
       return launch_bca_fwd2<Plan2<T, 256, 16, 16, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
-    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, sizeof(T) == 2 ? 2 : 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
+    case 512: return launch_bca_fwd2<Plan2<T, 512, 32, 16, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);  // (2-deep / no
+              // staging / 2 pipes measured equal or slower at q = 3, 4)
     // p = 2048 / 4096 (the paper's p sweep at D = 4096): the 2-pass plan with 64-point
     // register blocks (Plan2 R = 64), q * q <= VT weight spectra resident
     case 2048:
