@@ -135,8 +135,12 @@ int bca_bwd_accum(const void* x, const void* w, const void* g, void* dx, float* 
  *       of an fp32 copy of w), read only; the kernels skip their weight transform.
  *   bca_fwd_spectral:  y = IrdFFT(sum_j W_ij (.) X_j)  (accumulate != 0: y += ...)
  *   bca_bwd_spectral:  dx as bca_bwd (dx may alias g iff d_in == d_out), and
- *       dW = sum_t conj(X_tj) (.) G_ti as fp32 PACKED SPECTRA, no inverse — the
- *       gradient with respect to W (accumulate != 0: added to dW's contents).
+ *       dW = sum_t conj(X_tj) (.) G_ti as fp32 PACKED SPECTRA, no inverse (accumulate
+ *       != 0: added to dW's contents).  dW is rdFFT(dL/dw), the rdFFT of the
+ *       time-domain weight gradient: the update of spectral-domain SGD
+ *       (W -= lr dW, rdfft_packed_axpy; identical to time-domain SGD on w).  It is
+ *       NOT dL/dW — the packed slots of W are not independent coordinates of w;
+ *       dL/dW would weight slots 0 and p/2 by 1/p and every other slot by 2/p.
  *   Other arguments, layouts and errors as bca_fwd / bca_bwd.                 */
 int bca_fwd_spectral(const void* x, const float* W, void* y, int64_t T, int64_t d_in, int64_t d_out, int64_t p,
                      int dtype, int accumulate, void* stream);
@@ -173,6 +177,32 @@ int rdfft_packed_axpy(void* y, const void* x, float alpha, int64_t batch, int64_
 
 /* Static, never-allocating description of a status code. */
 const char* rdfft_status_str(int status);
+
+/* rdfft_filter_host — the transform path end to end from HOST memory: every
+ * row of xh becomes IrdFFT(rdFFT(row) (.) filt) (filt = NULL: the plain round
+ * trip IrdFFT(rdFFT(row)); conj != 0: (.) conj(filt)), the circular
+ * convolution of the row with the filter's impulse response (P:L165-172 with
+ * one block; P:L290-293 for the product).
+ *   xh:     HOST [batch][n] in/out.  Pinned (cudaHostAlloc / torch pin_memory)
+ *           for the copies to overlap the kernels; pageable memory is correct
+ *           but serialises.
+ *   filt:   DEVICE [n] packed spectrum (one row, broadcast), or NULL.
+ *   work:   DEVICE buffer of work_rows rows of n elements (caller-owned
+ *           workspace, work_rows >= 2): two halves that alternate between
+ *           stream0 and stream1.
+ *   Chunk c of at most work_rows/2 rows runs on stream (c % 2) through half
+ *   (c % 2): cudaMemcpyAsync host -> device, rdfft_fwd, rdfft_packed_mul
+ *   (if filt), rdfft_inv, cudaMemcpyAsync device -> host.  Consecutive chunks
+ *   on the two streams overlap their copies (both PCIe directions) with the
+ *   other chunk's kernels; the same half is reused only in its own stream's
+ *   order, so no event is needed.  Asynchronous: xh holds the result once both
+ *   streams have drained (the caller synchronises them; the streams must
+ *   already be ordered after the caller's earlier work on xh / filt / work).
+ *   stream0 == stream1 is allowed (no overlap).  No allocation.
+ *   Errors: as rdfft_fwd / rdfft_packed_mul, E_SHAPE for work_rows < 2,
+ *   E_ALIAS if filt overlaps work, E_CUDA if a copy cannot be enqueued.      */
+int rdfft_filter_host(void* xh, int64_t batch, int64_t n, int dtype, const void* filt, int conj, void* work,
+                      int64_t work_rows, void* stream0, void* stream1);
 
 /* Number of kernels this library has launched since load (process-wide,
  * monotonically increasing).  Used by bench.py to count its GPU launches.   */

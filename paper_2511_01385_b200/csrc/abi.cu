@@ -37,11 +37,11 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 }
 size_t dsize(int dtype) { return dtype == RDFFT_BF16 ? 2 : 4; }
 
-int num_sms() {
-  static int sms = 0;
+int num_sms() {  // per device (a process may drive several GPUs)
+  static int sms_dev[kMaxDevices] = {};
+  const int dev = device_index();
+  int& sms = sms_dev[dev];
   if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
@@ -53,18 +53,13 @@ int launched(int count = 1) {
   return cudaGetLastError() == cudaSuccess ? RDFFT_OK : RDFFT_E_CUDA;
 }
 
+// Every legal n has a specialised kernel (plan3.cuh dispatch); a launcher that could not launch
+// (e.g. cudaLaunchKernelEx of the n = 65536 cluster pair failed) is reported, never replaced.
 template <typename T>
 int launch_transform(T* x, int64_t batch, int n, bool inverse, cudaStream_t st) {
-  const int logn = ilog2(n);
-  if (launch_rdfft_fast<T>(x, batch, n, logn, inverse, num_sms(), st)) return launched();
-  const int V = kV1TileElems >> logn;
-  const int64_t tiles = (batch + V - 1) / V;
-  const int grid = (int)std::min<int64_t>(tiles, (int64_t)num_sms() * 8);
-  if (inverse)
-    rdfft_v1_kernel<T, true><<<grid, kV1Threads, 0, st>>>(x, batch, n, logn);
-  else
-    rdfft_v1_kernel<T, false><<<grid, kV1Threads, 0, st>>>(x, batch, n, logn);
-  return launched();
+  if (launch_rdfft_fast<T>(x, batch, n, ilog2(n), inverse, num_sms(), st)) return launched();
+  (void)cudaGetLastError();
+  return RDFFT_E_CUDA;
 }
 
 int transform(void* x, int64_t batch, int64_t n, int dtype, void* stream, bool inverse) {
@@ -435,6 +430,37 @@ int bca_bwd_spectral(const void* x, const float* W, const void* g, void* dx, flo
   return bca_bwd_impl(x, nullptr, g, dx, dW, T, d_in, d_out, p, dtype, stream, accumulate != 0, W, true);
 }
 
+int rdfft_filter_host(void* xh, int64_t batch, int64_t n, int dtype, const void* filt, int conj, void* work,
+                      int64_t work_rows, void* stream0, void* stream1) {
+  if (dtype != RDFFT_F32 && dtype != RDFFT_BF16) return RDFFT_E_DTYPE;
+  if (!pow2_transform(n)) return RDFFT_E_SIZE;
+  if (batch < 0 || work_rows < 2) return RDFFT_E_SHAPE;
+  if (batch == 0) return RDFFT_OK;
+  if (!xh || !work) return RDFFT_E_NULL;
+  if (!aligned16(work) || (filt && !aligned16(filt))) return RDFFT_E_ALIGN;
+  const size_t s = dsize(dtype);
+  const int64_t half = work_rows / 2;
+  const size_t row_bytes = (size_t)n * s;
+  if (filt && overlap(filt, row_bytes, work, (size_t)work_rows * row_bytes)) return RDFFT_E_ALIAS;
+  cudaStream_t st[2] = {static_cast<cudaStream_t>(stream0), static_cast<cudaStream_t>(stream1)};
+  char* host = static_cast<char*>(xh);
+  int rc = RDFFT_OK;
+  for (int64_t lo = 0, c = 0; lo < batch; lo += half, ++c) {
+    const int64_t rows = batch - lo < half ? batch - lo : half;
+    cudaStream_t sc = st[c & 1];
+    char* dev = static_cast<char*>(work) + (size_t)(c & 1) * half * row_bytes;
+    const size_t bytes = (size_t)rows * row_bytes;
+    if (cudaMemcpyAsync(dev, host + (size_t)lo * row_bytes, bytes, cudaMemcpyHostToDevice, sc) != cudaSuccess)
+      return RDFFT_E_CUDA;
+    if ((rc = transform(dev, rows, n, dtype, sc, false)) != RDFFT_OK) return rc;
+    if (filt && (rc = packed(dev, filt, rows, n, 1, dtype, sc, conj != 0)) != RDFFT_OK) return rc;
+    if ((rc = transform(dev, rows, n, dtype, sc, true)) != RDFFT_OK) return rc;
+    if (cudaMemcpyAsync(host + (size_t)lo * row_bytes, dev, bytes, cudaMemcpyDeviceToHost, sc) != cudaSuccess)
+      return RDFFT_E_CUDA;
+  }
+  return RDFFT_OK;
+}
+
 const char* rdfft_status_str(int status) {
   switch (status) {
     case RDFFT_OK: return "ok";
@@ -451,6 +477,6 @@ const char* rdfft_status_str(int status) {
 
 uint64_t rdfft_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
-int rdfft_abi_version(void) { return 103; }
+int rdfft_abi_version(void) { return 104; }
 
 }  // extern "C"

@@ -220,26 +220,6 @@ bool launch_bca_fwd5(const typename P::elem* x, const typename P::elem* w, typen
   return true;
 }
 
-// p = 1024 bf16: W spectra in TMEM + staged pipes (bca_fwd5); RDFFT_BCA_FWD5=0 falls back to fwd4.
-inline bool use_fwd5() {
-  static const bool v = [] {
-    const char* e = std::getenv("RDFFT_BCA_FWD5");
-    return !(e && *e == '0');
-  }();
-  return v;
-}
-
-// bf16: the 2-pipe kernel (LLaMA shape 0.190 -> 0.163 ms measured); fp32 keeps the staged
-// single-pipe kernel (its 8-byte direct loads made the 2-pipe variant slower: 0.194 -> 0.205 ms).
-// RDFFT_BCA_FWD4=0 selects the single-pipe kernel for bf16 too, for comparison.
-inline bool use_fwd4() {
-  static const bool v = [] {
-    const char* e = std::getenv("RDFFT_BCA_FWD4");
-    return !(e && *e == '0');
-  }();
-  return v;
-}
-
 #ifndef RDFFT_BCA_FWD_VT
 #define RDFFT_BCA_FWD_VT 16   // p = 1024 forward: 32 vectors (8 tokens of q = 4) per tile, 512 threads
 #endif
@@ -266,10 +246,10 @@ bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cu
       if constexpr (Q == 2) return launch_bca_fwd2<Plan2<T, 4096, 64, 4, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
       return false;
     case 1024:
-      if constexpr (sizeof(T) == 2) {
-        if (use_fwd5()) return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc, wspec);
-        if (use_fwd4()) return launch_bca_fwd4<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc, wspec);
-      }
+      // bf16: W spectra in tensor memory + two staged pipes (bca_fwd5); fp32 keeps the single-pipe
+      // kernel (its 8-byte direct loads made the 2-pipe variant slower: 0.194 -> 0.205 ms)
+      if constexpr (sizeof(T) == 2)
+        return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc, wspec);
       return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
           x, w, y, T_, sms, st, acc, wspec);
     default: return false;

@@ -249,42 +249,26 @@ bool launch_bca_bwd5(const typename P::elem* x, const typename P::elem* w, const
   return true;
 }
 
-// RDFFT_BCA_BWD5=0 selects bca_bwd4 for p = 1024 bf16.
-inline bool use_bwd5() {
-  static const bool v = [] {
-    const char* e = std::getenv("RDFFT_BCA_BWD5");
-    return !(e && *e == '0');
-  }();
-  return v;
-}
-
-// Measured (B200, T = 16384, bf16): LLaMA shape (p = 1024, q = 4) 0.319 -> 0.300 ms, RoBERTa-large
-// (p = 256, q = 4) 0.110 -> 0.097 ms; RoBERTa-base (p = 256, q = 3) 0.073 -> 0.103 ms (kept on bwd2).
-// RDFFT_BCA_BWD4=0 selects the previous kernels (bca_bwd2 / bca_bwd3) for comparison.
-inline bool use_bwd4() {
-  static const bool v = [] {
-    const char* e = std::getenv("RDFFT_BCA_BWD4");
-    return !(e && *e == '0');
-  }();
-  return v;
-}
-
+// Measured (B200, T = 16384, bf16): LLaMA shape (p = 1024, q = 4) bwd4 0.319 -> 0.300 ms over bwd2 and
+// bwd5 (W in TMEM) 0.276 ms; RoBERTa-large (p = 256, q = 4) 0.110 -> 0.097 ms; p = 256 runs bwd3.
+// The pair-split kernel (bwd4) only for even q (odd q: half the pair-split product is predicated off).
 template <typename T, int Q>
 bool bca_bwd_fast_q(const T* x, const T* w, const T* g, T* dx, float* dw, int64_t T_, int p, int sms,
                     cudaStream_t st, const float* wspec) {
-  const bool v4 = use_bwd4() && Q % 2 == 0;  // odd q: half the pair-split product is predicated off
   switch (p) {
     case 256:  // the single-group kernel (all threads in every phase): RoBERTa-base bf16 bwd 0.073 -> 0.061 ms,
                // RoBERTa-large 0.098 -> 0.081 ms (the 2-group / pair-split kernels measured slower here)
       return launch_bca_bwd3<Plan2<T, 256, 16, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
     case 512:  // (the single-group kernel measured slower here: 0.171 -> 0.200 ms at q = 4)
-      if (v4) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
-      return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      if constexpr (Q % 2 == 0) return launch_bca_bwd4<Plan2<T, 512, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      else return launch_bca_bwd2<Plan2<T, 512, 32, 8>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
     case 1024:
       if constexpr (sizeof(T) == 2 && Q % 2 == 0)
-        if (use_bwd5()) return launch_bca_bwd5<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
-      if (v4) return launch_bca_bwd4<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
-      return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+        return launch_bca_bwd5<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      else if constexpr (Q % 2 == 0)
+        return launch_bca_bwd4<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
+      else
+        return launch_bca_bwd3<Plan2<T, 1024, 32, 16>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
     case 2048:  // see bca_fwd_fast_q
       if constexpr (Q <= 2) return launch_bca_bwd3<Plan2<T, 2048, 64, 4>, Q>(x, w, g, dx, dw, T_, sms, st, wspec);
       return false;

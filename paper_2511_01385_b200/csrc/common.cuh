@@ -23,6 +23,16 @@ inline bool verbose() {
   return v;
 }
 
+// Kernel attributes (max dynamic shared memory, carveout) and occupancy are per device: the
+// launchers cache them per device index, so a second GPU driven from the same process is
+// configured on its first launch too.
+constexpr int kMaxDevices = 64;
+inline int device_index() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
 constexpr int kMaxN = 4096;
 constexpr int kMaxLogN = 12;
 

@@ -1,38 +1,10 @@
-// kernels_v1.cuh — straightforward shared-memory rdFFT kernels (one barrier per
-// stage).  Correctness baseline and fallback for shapes the register-blocked
-// kernels do not specialise; every entry still runs entirely on the GPU.
+// kernels_v1.cuh — packed (conj-)multiply kernels: the TMA-ring kernel for n >= 16
+// and a plain staged kernel for n < 16.
 #pragma once
 
 #include "stages.cuh"
 
 namespace rdfft {
-
-constexpr int kV1Threads = 256;
-constexpr int kV1TileElems = 4096;  // fp32 elements of smem per tile
-
-// One CTA transforms tiles of V = kV1TileElems / n vectors (grid-stride).
-template <typename T, bool kInverse>
-__global__ void __launch_bounds__(kV1Threads) rdfft_v1_kernel(T* __restrict__ x, int64_t batch, int n,
-                                                                int logn) {
-  __shared__ float s[kV1TileElems];
-  __shared__ float2 tw[kMaxN / 2];
-  make_twiddles(tw, n);
-  const int V = kV1TileElems >> logn;
-  const int64_t ntiles = (batch + V - 1) / V;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t v0 = tile * V;
-    const int nv = (int)(batch - v0 < V ? batch - v0 : V);
-    T* g = x + v0 * n;
-    __syncthreads();  // twiddles ready / previous tile's smem reads done
-    load_rows<T>(g, s, nv * n, n, logn, /*rev=*/!kInverse);
-    __syncthreads();
-    if (kInverse)
-      inv_stages_smem(s, nv, n, logn, tw);
-    else
-      fwd_stages_smem(s, nv, n, logn, tw);
-    store_rows<T>(g, s, nv * n, n, logn, /*rev=*/kInverse);
-  }
-}
 
 // a <- a (.) b or a (.) conj(b) per bin; b broadcast when b_batch == 1.
 // One CTA row-loop: rows are staged through shared memory with 16-byte global accesses,

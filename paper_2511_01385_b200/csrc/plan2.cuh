@@ -637,7 +637,8 @@ bool launch_plan2_dir(typename P::elem* x, int64_t batch, int sms, cudaStream_t 
   using L = P2Smem<P>;
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
   auto k = rdfft2_kernel<P, kInv>;
-  static int per_sm = 0;
+  static int per_sm_dev[kMaxDevices] = {};
+  int& per_sm = per_sm_dev[device_index()];
   if (!per_sm) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

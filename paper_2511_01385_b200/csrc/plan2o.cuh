@@ -141,7 +141,8 @@ bool launch_plan2o_inv(__nv_bfloat16* x, int64_t batch, int sms, cudaStream_t st
   using L = P2Smem<P>;
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
   auto k = rdfft2o_inv_kernel<P>;
-  static int per_sm = 0;
+  static int per_sm_dev[kMaxDevices] = {};
+  int& per_sm = per_sm_dev[device_index()];
   if (!per_sm) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

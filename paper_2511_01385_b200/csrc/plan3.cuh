@@ -538,9 +538,9 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
   auto kf = rdfft3_kernel<P, false>;
   auto ki = rdfft3_kernel<P, true>;
-  static bool configured = false;
-  static int per_sm = 1;
-  if (!configured) {
+  static int per_sm_dev[kMaxDevices] = {};
+  int& per_sm = per_sm_dev[device_index()];
+  if (!per_sm) {
     for (auto k : {kf, ki}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -550,7 +550,6 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ki, P::NT, L::BYTES);
     per_sm = a < b ? a : b;
     if (per_sm < 1) per_sm = 1;
-    configured = true;
     if (verbose())
       std::fprintf(stderr, "[rdfft] plan3 n=%d VT=%d NSTG=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N, P::VT,
                    P::NSTG, (size_t)L::BYTES, P::NT, per_sm);
@@ -569,25 +568,17 @@ bool launch_plan3(typename P::elem* x, int64_t batch, bool inverse, int sms, cud
 #endif
 // Returns true when a specialised kernel was launched for (n, T).
 // bf16 inverse, n = 128..1024: the staged-read kernel (plan2o.cuh; measured 64 -> 70-76 % of HBM at
-// 512/1024); everything else plan2 (the plan2o forward measured slower).  RDFFT_PLAN2O=0 forces plan2.
+// 512/1024); everything else plan2 (the plan2o forward measured slower).
 template <typename T, int N, int R, int VT>
 bool launch_p2(T* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
   if constexpr (sizeof(T) == 2 && N >= 512) {
-    static const bool use_o = [] {
-      const char* e = std::getenv("RDFFT_PLAN2O");
-      return !(e && *e == '0');
-    }();
     // n = 512: 2-deep TMA ring (0.71 -> 0.74 of HBM; at 1024 it costs a CTA per SM: 0.77 -> 0.75)
-    if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, (N == 512 ? 2 : 1)>>(x, batch, sms, st);
+    if (inverse) return launch_plan2o_inv<Plan2o<N, R, VT, (N == 512 ? 2 : 1)>>(x, batch, sms, st);
   }
   // bf16 n = 128 / 256: the staged-read inverse too (with the per-width staging skew it measured
   // 0.47 -> 0.51 / 0.60 -> 0.68 of HBM; n = 256 with a 2-deep staging ring)
   if constexpr (sizeof(T) == 2 && N >= 128 && N < 512) {
-    static const bool use_o = [] {
-      const char* e = std::getenv("RDFFT_PLAN2O");
-      return !(e && *e == '0');
-    }();
-    if (inverse && use_o) return launch_plan2o_inv<Plan2o<N, R, VT, (N == 256 ? 2 : 1)>>(x, batch, sms, st);
+    if (inverse) return launch_plan2o_inv<Plan2o<N, R, VT, (N == 256 ? 2 : 1)>>(x, batch, sms, st);
   }
   return launch_plan2<Plan2<T, N, R, VT, (N >= 512 ? RDFFT_FWD_NSTG : 2)>, Plan2<T, N, R, VT, (N >= 512 ? 1 : 2)>>(
       x, batch, inverse, sms, st);

@@ -522,7 +522,8 @@ template <typename P>
 bool launch_planl(typename P::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
   auto kf = rdfftl_kernel<P, false>;
   auto ki = rdfftl_kernel<P, true>;
-  static int per_sm = 0;
+  static int per_sm_dev[kMaxDevices] = {};
+  int& per_sm = per_sm_dev[device_index()];
   if (!per_sm) {
     for (auto k : {kf, ki}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::BYTES);
@@ -550,7 +551,8 @@ template <typename P>
 bool launch_planl_pair(typename P::elem* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
   auto kf = rdfftl_kernel<P, false, 2>;
   auto ki = rdfftl_kernel<P, true, 2>;
-  static bool configured = false;
+  static bool configured_dev[kMaxDevices] = {};
+  bool& configured = configured_dev[device_index()];
   if (!configured) {
     for (auto k : {kf, ki}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::BYTES2);

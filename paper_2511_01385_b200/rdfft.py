@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("RDFFT_LIB") or os.path.join(_HERE, "librdfft.so")  # RDFFT_LIB: A/B variants
+LIB_PATH = os.path.join(_HERE, "librdfft.so")
 
 F32, BF16 = 0, 1
 _DT = {torch.float32: F32, torch.bfloat16: BF16}
@@ -51,11 +51,12 @@ def _lib():
         lib.rdfft_encode.argtypes = [vp, vp, i64, i64, i32, vp]
         lib.rdfft_packed_conj.argtypes = [vp, i64, i64, i32, vp]
         lib.rdfft_packed_axpy.argtypes = [vp, vp, ctypes.c_float, i64, i64, i64, i32, vp]
+        lib.rdfft_filter_host.argtypes = [vp, i64, i64, i32, vp, i32, vp, i64, vp, vp]
         for f in ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum",
                   "bca_fwd_spectral", "bca_bwd_spectral",
                   "bca_bwd",
                   "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
-                  "rdfft_abi_version"):
+                  "rdfft_filter_host", "rdfft_abi_version"):
             getattr(lib, f).restype = i32
         lib.rdfft_status_str.argtypes = [i32]
         lib.rdfft_status_str.restype = ctypes.c_char_p
@@ -67,7 +68,7 @@ def _lib():
 EXPORTS = ("rdfft_fwd", "rdfft_inv", "rdfft_packed_mul", "rdfft_packed_conjmul", "bca_fwd", "bca_fwd_accum", "bca_bwd",
            "bca_fwd_spectral", "bca_bwd_spectral",
            "bca_bwd_accum", "rdfft_decode", "rdfft_encode", "rdfft_packed_conj", "rdfft_packed_axpy",
-           "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
+           "rdfft_filter_host", "rdfft_status_str", "rdfft_launch_count", "rdfft_abi_version")
 
 
 def _ptr(t):
@@ -90,6 +91,32 @@ def _check(t, name):
         raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+
+
+def _same_dtype(ref, **ts):
+    for name, t in ts.items():
+        if t is not None and t.dtype != ref.dtype:
+            raise ValueError(f"{name} has dtype {t.dtype}, expected {ref.dtype} (x's dtype)")
+
+
+def _numel(t, want, name):
+    if t.numel() != want:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {want}")
+
+
+def _f32(t, name):
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be float32 (P:L486), got {t.dtype}")
+
+
+def _weights(w, name, x=None):
+    """(q_out, q_in, p) of a weight tensor [q_out, q_in, p]; checks x's last dimension is q_in * p."""
+    if w.dim() != 3:
+        raise ValueError(f"{name} must be [q_out, q_in, p], got shape {tuple(w.shape)}")
+    q_out, q_in, p = w.shape
+    if x is not None and x.shape[-1] != q_in * p:
+        raise ValueError(f"x last dim {x.shape[-1]} != q_in*p = {q_in * p}")
+    return q_out, q_in, p
 
 
 def _call(fn, *args):
@@ -140,17 +167,16 @@ def bca_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor | None = None, acc
     output W0 x in the same pass."""
     _check(x, "x")
     _check(w, "w")
-    q_out, q_in, p = w.shape
+    q_out, q_in, p = _weights(w, "w", x)
     d_in, d_out = q_in * p, q_out * p
-    if x.shape[-1] != d_in:
-        raise ValueError(f"x last dim {x.shape[-1]} != q_in*p = {d_in}")
+    rows = x.numel() // d_in
     if y is None:
         if accumulate:
             raise ValueError("accumulate=True needs the y to add into")
         y = torch.empty(x.shape[:-1] + (d_out,), dtype=x.dtype, device=x.device)
     _check(y, "y")
-    if w.dtype != x.dtype or y.dtype != x.dtype:
-        raise ValueError("x, w, y must share a dtype")
+    _same_dtype(x, w=w, y=y)
+    _numel(y, rows * d_out, "y")
     _call("bca_fwd_accum" if accumulate else "bca_fwd", _ptr(x), _ptr(w), _ptr(y), x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
     return y
 
@@ -163,8 +189,9 @@ def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor 
     _check(x, "x")
     _check(w, "w")
     _check(g, "g")
-    q_out, q_in, p = w.shape
+    q_out, q_in, p = _weights(w, "w", x)
     d_in, d_out = q_in * p, q_out * p
+    rows = x.numel() // d_in
     if dx is None:
         dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
     if dw is None:
@@ -173,8 +200,11 @@ def bca_bwd(x: torch.Tensor, w: torch.Tensor, g: torch.Tensor, dx: torch.Tensor 
         dw = torch.empty((q_out, q_in, p), dtype=torch.float32, device=x.device)
     _check(dx, "dx")
     _check(dw, "dw")
-    if dw.dtype != torch.float32:
-        raise ValueError("dw must be float32 (P:L486)")
+    _same_dtype(x, w=w, g=g, dx=dx)
+    _f32(dw, "dw")
+    _numel(g, rows * d_out, "g")
+    _numel(dx, rows * d_in, "dx")
+    _numel(dw, q_out * q_in * p, "dw")
     _call("bca_bwd_accum" if accumulate else "bca_bwd", _ptr(x), _ptr(w), _ptr(g), _ptr(dx), _ptr(dw),
           x.numel() // d_in, d_in, d_out, p, _dtype(x), _stream(x))
     return dx, dw
@@ -185,17 +215,17 @@ def bca_fwd_spectral(x: torch.Tensor, W: torch.Tensor, y: torch.Tensor | None = 
     """y = BCA(x) from resident weight spectra W (fp32 [q_out, q_in, p], packed: rdfft_fwd of w)."""
     _check(x, "x")
     _check(W, "W")
-    if W.dtype != torch.float32:
-        raise ValueError("W (weight spectra) must be float32")
-    q_out, q_in, p = W.shape
+    _f32(W, "W (weight spectra)")
+    q_out, q_in, p = _weights(W, "W", x)
     d_in, d_out = q_in * p, q_out * p
-    if x.shape[-1] != d_in:
-        raise ValueError(f"x last dim {x.shape[-1]} != q_in*p = {d_in}")
+    rows = x.numel() // d_in
     if y is None:
         if accumulate:
             raise ValueError("accumulate=True needs the y to add into")
         y = torch.empty(x.shape[:-1] + (d_out,), dtype=x.dtype, device=x.device)
     _check(y, "y")
+    _same_dtype(x, y=y)
+    _numel(y, rows * d_out, "y")
     _call("bca_fwd_spectral", _ptr(x), _ptr(W), _ptr(y), x.numel() // d_in, d_in, d_out, p, _dtype(x),
           int(accumulate), _stream(x))
     return y
@@ -203,12 +233,17 @@ def bca_fwd_spectral(x: torch.Tensor, W: torch.Tensor, y: torch.Tensor | None = 
 
 def bca_bwd_spectral(x: torch.Tensor, W: torch.Tensor, g: torch.Tensor, dx: torch.Tensor | None = None,
                      dW: torch.Tensor | None = None, accumulate: bool = False):
-    """(dx, dW) with dW the fp32 packed-spectrum gradient of the resident spectra W (no inverse)."""
+    """(dx, dW) for resident weight spectra W.  dW = sum_t conj(X_t) (.) G_t in the packed layout, i.e.
+    rdFFT of the time-domain gradient dL/dw (no inverse) — the update of spectral SGD, W -= lr * dW
+    (equivalent to time-domain SGD on w).  It is NOT dL/dW: the packed entries of W are not
+    independent parameters of w (dL/dW would weight the DC / Nyquist slots by 1/p and the rest by 2/p)."""
     _check(x, "x")
     _check(W, "W")
     _check(g, "g")
-    q_out, q_in, p = W.shape
+    _f32(W, "W (weight spectra)")
+    q_out, q_in, p = _weights(W, "W", x)
     d_in, d_out = q_in * p, q_out * p
+    rows = x.numel() // d_in
     if dx is None:
         dx = torch.empty(x.shape, dtype=x.dtype, device=x.device)
     if dW is None:
@@ -217,6 +252,11 @@ def bca_bwd_spectral(x: torch.Tensor, W: torch.Tensor, g: torch.Tensor, dx: torc
         dW = torch.empty((q_out, q_in, p), dtype=torch.float32, device=x.device)
     _check(dx, "dx")
     _check(dW, "dW")
+    _same_dtype(x, g=g, dx=dx)
+    _f32(dW, "dW")
+    _numel(g, rows * d_out, "g")
+    _numel(dx, rows * d_in, "dx")
+    _numel(dW, q_out * q_in * p, "dW")
     _call("bca_bwd_spectral", _ptr(x), _ptr(W), _ptr(g), _ptr(dx), _ptr(dW), x.numel() // d_in, d_in, d_out, p,
           _dtype(x), int(accumulate), _stream(x))
     return dx, dW
@@ -267,6 +307,37 @@ def rdfft_packed_axpy(y: torch.Tensor, x: torch.Tensor, alpha: float) -> torch.T
     _call("rdfft_packed_axpy", _ptr(y), _ptr(x), float(alpha), y.numel() // n, n, x.numel() // n, _dtype(y),
           _stream(y))
     return y
+
+
+def rdfft_filter_host(xh: torch.Tensor, work: torch.Tensor, filt: torch.Tensor | None = None, conj: bool = False,
+                      streams=None) -> torch.Tensor:
+    """In place on the HOST rows of xh: xh <- IrdFFT(rdFFT(xh) (.) [conj] filt) (filt None: round trip),
+    streamed through the caller's device workspace `work` ([rows, n], rows >= 2) on two CUDA streams
+    (the C-ABI's rdfft_filter_host; copies overlap kernels).  The streams are ordered after torch's
+    current stream on entry, and torch's current stream waits for them on return (so a following
+    torch.cuda.synchronize() or current-stream op sees the finished xh)."""
+    if xh.is_cuda:
+        raise ValueError("xh must be a host tensor (pinned for overlap)")
+    if not xh.is_contiguous():
+        raise ValueError("xh must be contiguous")
+    _check(work, "work")
+    n = xh.shape[-1]
+    if work.dtype != xh.dtype or work.shape[-1] != n or work.numel() // n < 2:
+        raise ValueError("work must be a CUDA [rows >= 2, n] tensor of xh's dtype")
+    if filt is not None:
+        _check(filt, "filt")
+        if filt.dtype != xh.dtype or filt.numel() != n:
+            raise ValueError("filt must be one packed row [n] of xh's dtype")
+    cur = torch.cuda.current_stream(work.device)
+    streams = streams or [torch.cuda.Stream(work.device) for _ in range(2)]
+    for s in streams:
+        s.wait_stream(cur)
+    _call("rdfft_filter_host", ctypes.c_void_p(xh.data_ptr()), xh.numel() // n, n, _dtype(xh), _ptr(filt),
+          int(conj), _ptr(work), work.numel() // n, ctypes.c_void_p(streams[0].cuda_stream),
+          ctypes.c_void_p(streams[-1].cuda_stream))
+    for s in streams:
+        cur.wait_stream(s)
+    return xh
 
 
 def launch_count() -> int:

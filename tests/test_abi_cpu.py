@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(lib):
     from paper_2511_01385_b200 import rdfft
 
     assert set(rdfft.EXPORTS) == set(declared_functions())
-    assert lib.rdfft_abi_version() == 103
+    assert lib.rdfft_abi_version() == 104
 
 
 def test_status_strings(lib):
@@ -121,3 +121,51 @@ def test_oracle_not_imported_by_product_path():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b|#include\s+[<\"].*oracle", src, flags=re.M), f
+
+
+def test_filter_host_validation(lib):
+    h = ctypes.c_void_p(0x1000000)
+    work = ctypes.c_void_p(0x40000000)
+    f = lib.rdfft_filter_host
+    assert f(h, 4, 12, 0, None, 0, work, 4, None, None) == 1        # E_SIZE
+    assert f(h, 4, 8, 5, None, 0, work, 4, None, None) == 4         # E_DTYPE
+    assert f(h, 4, 8, 0, None, 0, work, 1, None, None) == 5         # work_rows < 2
+    assert f(h, -1, 8, 0, None, 0, work, 4, None, None) == 5        # negative batch
+    assert f(None, 4, 8, 0, None, 0, work, 4, None, None) == 2      # E_NULL (host)
+    assert f(h, 4, 8, 0, None, 0, None, 4, None, None) == 2         # E_NULL (work)
+    assert f(h, 4, 8, 0, None, 0, MIS, 4, None, None) == 3          # E_ALIGN
+    assert f(h, 4, 8, 0, ctypes.c_void_p(0x40000010), 0, work, 4, None, None) == 6  # filt inside work
+    assert f(None, 0, 8, 0, None, 0, None, 4, None, None) == 0      # batch 0: no-op
+
+
+def test_library_objects_call_no_allocator(lib):
+    """Zero intermediate allocation (north star), checked on what the library's own object
+    files can call: every CUDA / C runtime symbol they import is on an allowlist that holds no
+    allocator (no cudaMalloc*, cudaMallocAsync, cudaHostAlloc, cuMemAlloc*, cuMemCreate, malloc,
+    operator new).  The GPU test test_zero_allocation checks the same at run time through
+    cudaMemGetInfo and torch's allocator."""
+    import glob
+    import subprocess
+
+    objs = glob.glob(os.path.join(ROOT, "paper_2511_01385_b200", "build", "*.o"))
+    assert objs, "build/*.o missing (built by build.build())"
+    allowed = {"cudaDeviceGetAttribute", "cudaFuncSetAttribute", "cudaGetDevice", "cudaGetLastError",
+               "cudaLaunchKernel", "cudaLaunchKernelExC", "cudaMemsetAsync", "cudaMemcpyAsync",
+               "cudaOccupancyMaxActiveBlocksPerMultiprocessorWithFlags", "__cudaPopCallConfiguration",
+               "__cudaPushCallConfiguration", "__cudaRegisterFatBinary", "__cudaRegisterFatBinaryEnd",
+               "__cudaRegisterFunction", "__cudaRegisterVar", "__cudaUnregisterFatBinary", "_GLOBAL_OFFSET_TABLE_",
+               "__cxa_guard_acquire", "__cxa_guard_release", "__fprintf_chk", "__stack_chk_fail", "atexit",
+               "getenv", "stderr"}
+    seen = set()
+    for obj in objs:
+        out = subprocess.run(["nm", "-u", obj], capture_output=True, text=True, check=True).stdout
+        for line in out.splitlines():
+            sym = line.split()[-1]
+            if sym.startswith("_Z"):
+                dem = subprocess.run(["c++filt", sym], capture_output=True, text=True).stdout.strip()
+                assert not re.search(r"operator new|malloc|alloc", dem), (obj, dem)
+                continue
+            seen.add(sym)
+    bad = {s for s in seen if re.search(r"alloc|cuMem|Malloc|HostRegister", s, flags=re.I)}
+    assert not bad, bad
+    assert seen <= allowed, seen - allowed

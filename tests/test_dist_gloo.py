@@ -90,3 +90,20 @@ def test_two_rank_bca_dw_allreduce_and_sharding():
         xs = synth.randn((10, 16), seed=9).double().numpy()
         np.testing.assert_allclose(fwd_shard, o.rdfft_fwd(xs)[lo2:hi2], atol=1e-12)
     assert res[0][2] == res[1][1]  # token shards are contiguous and disjoint
+
+
+def test_chunked_generator_identical_for_any_sharding():
+    """configs[4] inputs (SURVEY §8(d) cfg 5): 64 fixed seeded chunks, so the global data a rank's
+    shard sees does not depend on how many ranks share the batch."""
+    from paper_2511_01385_b200 import synth
+
+    total, row = 1000, (8,)
+    full = synth.randn_rows(total, row, 0, total, seed=3, dtype="f32", chunks=64)
+    assert full.shape == (total, 8)
+    for world in (1, 2, 3, 8):
+        parts = [synth.randn_rows(total, row, *D.shard_range(total, r, world), seed=3, dtype="f32", chunks=64)
+                 for r in range(world)]
+        assert torch.equal(torch.cat(parts), full)
+    # pieces are distinct streams (seed + c), not one stream cut up
+    lo, hi = synth.chunk_range(total, 1, 64)
+    assert torch.equal(full[lo:hi], synth.randn((hi - lo,) + row, seed=4, dtype="f32"))

@@ -74,11 +74,11 @@ def test_single_layer_peak_memory(B_, D, p):
 
     Beyond x, w and grad_output the fused path may allocate exactly y (forward)
     and the fp32 dw (+ its cast for bf16 parameters) - no spectra, no complex
-    intermediates; dx reuses grad_output.  autograd's AccumulateGrad may
-    copy dx into x.grad because the caller still holds g: one more [B, D] block,
-    which is not the layer's."""
+    intermediates; with the opt-in inplace_grad dx reuses grad_output.
+    autograd's AccumulateGrad may copy dx into x.grad because the caller still
+    holds g: one more [B, D] block, which is not the layer's."""
     dt = torch.bfloat16
-    layer = B.BlockCirculantAdapter(D, D, p, dtype=dt, device="cuda")
+    layer = B.BlockCirculantAdapter(D, D, p, dtype=dt, device="cuda", inplace_grad=True)
     x = torch.randn(B_, D, device="cuda", dtype=dt, requires_grad=True)
     g = torch.randn(B_, D, device="cuda", dtype=dt)
     torch.cuda.synchronize()
@@ -116,3 +116,64 @@ def test_adapter_on_frozen_path_grads(dtype, tol):
     dxo, dwo = o.bca_bwd(xo, wo, go)
     assert rel(f64(xc.grad), dxo + go @ w0o) <= tol
     assert rel(f64(layer.weight.grad), dwo) <= (1e-5 if dtype == "f32" else 2e-2)
+
+
+@pytest.mark.parametrize("dtype,tol", [("f32", 1e-5), ("bf16", 2e-2)])
+def test_shared_grad_output_not_clobbered(dtype, tol):
+    """AddBackward hands ONE grad tensor to both branches of linear(x) + adapter(x) and of a
+    residual h + adapter(h); the adapter's backward (run first) must not overwrite it.
+    Default mode: dx in its own buffer, grads match the oracle, the caller's g is untouched."""
+    T, q, p = 33, 2, 256
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=17, dtype=dtype)
+    w0 = (synth.randn((q * p, q * p), seed=18, dtype="f32") * (q * p) ** -0.5).to(x.dtype)
+    layer = B.BlockCirculantAdapter(q * p, q * p, p, dtype=x.dtype, device="cuda")
+    with torch.no_grad():
+        layer.weight.copy_(w.cuda())
+    xo, wo, go, w0o = f64(x), f64(w), f64(g), f64(w0)
+    dxo, dwo = o.bca_bwd(xo, wo, go)
+    # linear(x) + adapter(x)
+    xc = x.cuda().requires_grad_(True)
+    gc = g.cuda()
+    g_before = gc.clone()
+    y = xc @ w0.cuda().t() + layer(xc)
+    y.backward(gc)
+    torch.cuda.synchronize()
+    assert torch.equal(gc, g_before)
+    assert rel(f64(xc.grad), dxo + go @ w0o) <= tol
+    assert rel(f64(layer.weight.grad), dwo) <= tol
+    # residual h + adapter(h)
+    layer.weight.grad = None
+    hc = x.cuda().requires_grad_(True)
+    y = hc + layer(hc)
+    y.backward(gc)
+    torch.cuda.synchronize()
+    assert torch.equal(gc, g_before)
+    assert rel(f64(hc.grad), dxo + go) <= tol
+    assert rel(f64(layer.weight.grad), dwo) <= tol
+
+
+def test_inplace_grad_opt_in_and_no_input_grad():
+    """inplace_grad=True writes dx over grad_output for a sole consumer; an input that does
+    not require grad gets None while w still gets its gradient."""
+    T, q, p = 21, 2, 128
+    x, w, g = synth.bca_inputs(T, q * p, q * p, p, seed=19, dtype="f32")
+    xo, wo, go = f64(x), f64(w), f64(g)
+    dxo, dwo = o.bca_bwd(xo, wo, go)
+    layer = B.BlockCirculantAdapter(q * p, q * p, p, device="cuda", inplace_grad=True)
+    with torch.no_grad():
+        layer.weight.copy_(w.cuda())
+    xc = x.cuda().requires_grad_(True)
+    gc = g.cuda()
+    layer(xc).backward(gc)
+    torch.cuda.synchronize()
+    assert rel(f64(xc.grad), dxo) <= 1e-5
+    assert rel(f64(gc), dxo) <= 1e-5  # grad_output now holds dx
+    layer.weight.grad = None
+    xf = x.cuda()  # no grad
+    layer2 = B.BlockCirculantAdapter(q * p, q * p, p, device="cuda")
+    with torch.no_grad():
+        layer2.weight.copy_(w.cuda())
+    y = layer2(xf)
+    y.backward(g.cuda())
+    assert xf.grad is None
+    assert rel(f64(layer2.weight.grad), dwo) <= 1e-5

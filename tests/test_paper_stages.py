@@ -73,3 +73,15 @@ def test_paper_index_example():
     b = np.array(ps.forward(list(x), stages=3))
     Y8 = np.fft.fft(x[0::2])  # window 0 of size 8 holds DFT of x[bitrev(0)::2] = x[0::2]
     assert abs(b[2] - Y8[2].real) < 1e-12 and abs(b[6] - Y8[2].imag) < 1e-12
+
+
+def test_bit_reverse_spec_goldens():
+    """The SPEC's bit-reversal examples (tests/golden/spec_worked_examples.json) pin the
+    permutation the staged re-derivation applies before the forward and after the inverse (C5)."""
+    import json
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "spec_worked_examples.json")) as f:
+        gold = json.load(f)["bit_reverse"]
+    assert gold
+    for case in gold:
+        assert ps.bit_reverse(list(case["in"])) == case["out"], case["cite"]
