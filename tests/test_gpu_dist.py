@@ -56,7 +56,10 @@ def _worker(rank, world, port, dtype, q):
         tlo, thi = Dd.shard_range(T, rank, world)
         f, x, y, dx, dw = _work(lo, hi, tlo, thi, dtype)
         Dd.allreduce_dw(dw)  # gloo all-reduce of the CUDA fp32 dw (NCCL on the 8-GPU box)
-        q.put((rank, lo, hi, tlo, thi, f, x, y, dx, dw.cpu()))
+        # numpy copies: pickled by value (torch CPU tensors would travel as shared-memory handles
+        # that die with this process)
+        q.put((rank, lo, hi, tlo, thi, *(t.float().numpy() if t.dtype == torch.bfloat16 else t.numpy()
+                                         for t in (f, x, y, dx, dw.cpu()))))
     finally:
         dist.destroy_process_group()
 
@@ -77,12 +80,14 @@ def test_two_rank_shards_bit_identical(cuda_device, dtype):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    f1, x1, y1, dx1, dw1 = _work(0, TOTAL, 0, T, dtype)
+    one = _work(0, TOTAL, 0, T, dtype)  # the 1-rank run
+    f1, x1, y1, dx1 = (t.float().numpy() for t in one[:4])
+    dw1 = one[4].cpu().double().numpy()
     for rank, lo, hi, tlo, thi, f, x, y, dx, dw in res:
-        assert torch.equal(f, f1[lo:hi])      # forward spectra: bit-identical rows
-        assert torch.equal(x, x1[lo:hi])      # fwd -> packed_mul -> inv: bit-identical rows
-        assert torch.equal(y, y1[tlo:thi])    # BCA forward per token
-        assert torch.equal(dx, dx1[tlo:thi])  # BCA dx per token (shard-local)
-        d, d1 = dw.double(), dw1.double().cpu()
-        assert float((d - d1).norm() / d1.norm()) <= 1e-5  # all-reduced dw vs 1-rank dw (fp32 gate)
-    assert res[0][2] == res[1][1] and res[0][4] == res[1][3]
+        # bf16 values widen exactly to fp32, so equality of the widened arrays is bit-equality
+        assert np.array_equal(f, f1[lo:hi])      # forward spectra: bit-identical rows
+        assert np.array_equal(x, x1[lo:hi])      # fwd -> packed_mul -> inv: bit-identical rows
+        assert np.array_equal(y, y1[tlo:thi])    # BCA forward per token
+        assert np.array_equal(dx, dx1[tlo:thi])  # BCA dx per token (shard-local)
+        assert np.linalg.norm(dw - dw1) / np.linalg.norm(dw1) <= 1e-5  # all-reduced vs 1-rank dw
+    assert res[0][2] == res[1][1] and res[0][4] == res[1][3]  # contiguous, disjoint shards
