@@ -49,7 +49,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *FLAGS, *inc, "-c", "-o", obj, src]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+        out = subprocess.run(cmd, capture_output=True, text=True)
+        if out.stdout or out.stderr:
+            print(out.stdout + out.stderr, end="", flush=True)
+        if out.returncode:
+            raise subprocess.CalledProcessError(out.returncode, cmd, out.stdout, out.stderr)
+        # zero local memory on every kernel (every instantiated kernel is on a dispatched path):
+        # a register spill fails the build (-Xptxas -warn-spills reports them)
+        spills = [ln for ln in out.stderr.splitlines() if "spilled to local memory" in ln]
+        if spills:
+            os.remove(obj)
+            raise RuntimeError(f"register spills in {os.path.basename(src)}:\n" + "\n".join(spills))
         return obj
 
     with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:

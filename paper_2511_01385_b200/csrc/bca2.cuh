@@ -454,12 +454,21 @@ int bca2_grid(K kernel, int threads, size_t smem, int64_t units, int sms) {
 template <typename P, int Q = kBcaQMax>
 struct BcaBwd3Smem {
   static constexpr int WF = bca_wrows<P, Q>() * P::ROWA + 16;
+  static constexpr int NI = P::N / 4;
+  static constexpr int IPT = NI > P::NT ? NI / P::NT : 1;  // product items per thread
+  // p = 2048 / 4096 (64-point register blocks, 4 or 8 items per thread): the dW accumulators
+  // (IPT q^2 bin pairs per thread) live in shared memory, one float4 per (item, i, j) per thread
+  // (thread-major: conflict-free 16-byte accesses), instead of registers that spilled
+  // (bf16 p = 4096: 255 registers + 268 B of local memory)
+  static constexpr bool ACC_SMEM = IPT >= 4;
   static constexpr size_t HX_OFF = 0;
   static constexpr size_t HG_OFF = HX_OFF + (size_t)P::HF * 8;
   static constexpr size_t W_OFF = HG_OFF + (size_t)P::HF * 8;
   static constexpr size_t TWF_OFF = W_OFF + (size_t)WF * 8;
   static constexpr size_t TWI_OFF = TWF_OFF + (size_t)P::TWF * 8;
-  static constexpr size_t BYTES = TWI_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t ACC_OFF = TWI_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t TMEM_OFF = ACC_OFF + (ACC_SMEM ? (size_t)IPT * Q * Q * P::NT * 16 : 0);
+  static constexpr size_t BYTES = TMEM_OFF + 16;  // + the TMEM address (bca_bwd4)
 };
 
 template <typename P, int Q>
@@ -482,14 +491,19 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
   float2* TWi = reinterpret_cast<float2*>(base + L::TWI_OFF);
   const int tid = threadIdx.x;
   const int TT = P::VT / q;
-  const int64_t ntiles = (T_ + TT - 1) / TT;
+  // 32-bit tile indices (T < 2^31 tokens): smaller loop state for the 64-point register blocks
+  const int ntiles = (int)((T_ + TT - 1) / TT);
   const int64_t tok_elems = (int64_t)q * N;
   p2_tables<P>(TWf, TWi, tid, NT);
   p2_zero_pads<P>(Hx, P::VT, tid, NT);
   p2_zero_pads<P>(Hg, P::VT, tid, NT);
   p2_zero_pads<P>(Wr, q * q, tid, NT);
   const uint32_t k65536 = kTwo16;
-  const P2Roles<P> rx(Hx, TWf, TWi, tid), rg(Hg, TWf, TWi, tid);
+  // one role set: the g group's H region is the x group's shifted by HF (Hg = Hx + HF), so rg is rx
+  // with an offset (a second set of role pointers cost ~20 live registers: spills at p = 2048 / 4096)
+  const P2Roles<P> rx(Hx, TWf, TWi, tid);
+  static_assert(L::HG_OFF == L::HX_OFF + (size_t)P::HF * 8, "Hg = Hx + HF");
+  constexpr int GOFF = P::HF;
   __syncthreads();
   if (wspec) {
     p2_load_spectra<P>(Wr, wspec, q * q, tid, NT);
@@ -504,23 +518,41 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
   static_assert(NT % NI == 0 || NI % NT == 0, "item mapping");
   constexpr int IPT = NI > NT ? NI / NT : 1;  // items per thread
   constexpr int TS = NT >= NI ? NT / NI : 1;   // token split
-  BinPair acc[IPT][Q][Q];
+  static_assert(IPT == L::IPT, "layout");
+  constexpr bool kAccS = L::ACC_SMEM;
+  float4* accS = reinterpret_cast<float4*>(base + L::ACC_OFF);  // [a][i][j][tid] (kAccS)
+  auto acc_slot = [&](int a, int i, int j) { return accS + ((a * Q + i) * Q + j) * NT + tid; };
+  BinPair acc[kAccS ? 1 : IPT][Q][Q];
 #pragma unroll
-  for (int a = 0; a < IPT; ++a)
+  for (int a = 0; a < (kAccS ? 1 : IPT); ++a)
 #pragma unroll
     for (int i = 0; i < Q; ++i)
 #pragma unroll
       for (int j = 0; j < Q; ++j) acc[a][i][j] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
+  if constexpr (kAccS) {
+#pragma unroll
+    for (int a = 0; a < IPT; ++a)
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+          if (i < q && j < q) *acc_slot(a, i, j) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ntok = (int)(T_ - (int64_t)tile * TT < TT ? T_ - (int64_t)tile * TT : TT);
     const int nv = ntok * q;
-    p2_pass1_fwd<P, true>(rx, x + tile * TT * tok_elems, nv, k65536);
-    p2_pass1_fwd<P, true>(rg, g + tile * TT * tok_elems, nv, k65536);
+    const int64_t e0 = (int64_t)tile * TT * tok_elems;
+    // (compiler fences between the two operands: interleaving two 64-point register FFTs would
+    // double the live registers at p = 2048 / 4096)
+    p2_pass1_fwd<P, true>(rx, x + e0, nv, k65536);
+    asm volatile("" ::: "memory");
+    p2_pass1_fwd<P, true>(rx, g + e0, nv, k65536, GOFF);
     __syncthreads();
     p2_last_fwd<P>(rx, nv);
-    p2_last_fwd<P>(rg, nv);
+    asm volatile("" ::: "memory");
+    p2_last_fwd<P>(rx, nv, GOFF);
     p2_dc_fwd<P>(rx, nv);
-    p2_dc_fwd<P>(rg, nv);
+    p2_dc_fwd<P>(rx, nv, GOFF);
     __syncthreads();
 #pragma unroll
     for (int a = 0; a < IPT; ++a) {
@@ -535,6 +567,17 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
 #pragma unroll
         for (int j = 0; j < Q; ++j)
           if (i < q && j < q) wv[i][j] = bins_get(Wr + P::row(i * q + j), oa, ob, special);
+      BinPair (&ac)[Q][Q] = acc[kAccS ? 0 : a];
+      if constexpr (kAccS) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+          for (int j = 0; j < Q; ++j)
+            if (i < q && j < q) {
+              const float4 f = *acc_slot(a, i, j);
+              ac[i][j] = {make_float2(f.x, f.y), make_float2(f.z, f.w)};
+            }
+      }
       for (int tt = ts; tt < ntok; tt += TS) {
         BinPair xv[Q], gv[Q];
 #pragma unroll
@@ -552,8 +595,8 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
 #pragma unroll
           for (int j = 0; j < Q; ++j)
             if (i < q && j < q) {
-              acc[a][i][j].b1 = pmac(xv[j].b1, g1[i], acc[a][i][j].b1);
-              acc[a][i][j].b2 = cfmac(xv[j].b2, gv[i].b2, acc[a][i][j].b2);
+              ac[i][j].b1 = pmac(xv[j].b1, g1[i], ac[i][j].b1);
+              ac[i][j].b2 = cfmac(xv[j].b2, gv[i].b2, ac[i][j].b2);
             }
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
@@ -569,12 +612,19 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
           }
         }
       }
+      if constexpr (kAccS) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+#pragma unroll
+          for (int j = 0; j < Q; ++j)
+            if (i < q && j < q) *acc_slot(a, i, j) = make_float4(ac[i][j].b1.x, ac[i][j].b1.y, ac[i][j].b2.x, ac[i][j].b2.y);
+      }
     }
     __syncthreads();
     p2_last_inv<P>(rx, nv);
     p2_dc_inv<P>(rx, nv);
     __syncthreads();
-    p2_pass1_inv<P>(rx, dx + tile * TT * tok_elems, nv);  // g rows of this tile are already consumed
+    p2_pass1_inv<P>(rx, dx + e0, nv);  // g rows of this tile are already consumed
     __syncthreads();
   }
 #pragma unroll
@@ -586,7 +636,13 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
       for (int j = 0; j < Q; ++j) {
         if (i < q && j < q) {
           float* d = dw + (int64_t)(i * q + j) * N;
-          const BinPair v = acc[a][i][j];
+          BinPair v;
+          if constexpr (kAccS) {
+            const float4 f = *acc_slot(a, i, j);
+            v = {make_float2(f.x, f.y), make_float2(f.z, f.w)};
+          } else {
+            v = acc[kAccS ? 0 : a][i][j];
+          }
           if (u == 0) {
             atomicAdd(d + 0, v.b1.x);
             atomicAdd(d + N / 2, v.b1.y);

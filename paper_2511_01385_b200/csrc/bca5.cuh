@@ -18,29 +18,6 @@
 
 namespace rdfft {
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
-               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-               : "memory");
-}
-// Wait for this thread's outstanding tcgen05.ld; the registers are in/out operands so no use of
-// them can be scheduled above the wait.
-__device__ __forceinline__ void tmem_wait_ld(uint32_t (&r)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-               :: "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
 template <typename P, int PIPES>
 struct BcaFwd5Smem {  // [stage x PIPES][H x PIPES][TWf][TWi][bars x PIPES][tmem addr]
   static constexpr size_t H_OFF = (size_t)PIPES * P::STAGE;
@@ -59,9 +36,10 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
   constexpr int q = Q;
   using T = typename P::elem;
   using L = BcaFwd5Smem<P, PIPES>;
-  constexpr int N = P::N, NT = P::NT, NI = N / 4;
-  static_assert(NT == NI && NI == 256, "one product item per thread, two items per TMEM lane");
-  static_assert(Q * Q <= P::VT && PIPES >= 2, "W prologue uses pipe 1's H region as scratch");
+  constexpr int N = P::N, NT = P::NT, NI = N / 4, IPT = NI / NT, VT = P::VT;
+  static_assert(NI == 256 && (NT == 256 || NT == 128), "one or two product items per thread, NT % 128 == 0");
+  // the W prologue transforms the q*q weight rows VT at a time in the H regions of pipes 1, 2, ...
+  static_assert(PIPES >= 1 + (Q * Q + VT - 1) / VT, "W prologue scratch: pipes 1.. hold q*q rows");
   constexpr uint32_t kCols = 128;
   extern __shared__ float4 smem4[];
   unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
@@ -74,7 +52,7 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF) + pipe;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::TMEM_OFF);
   unsigned char* stg = base + (size_t)pipe * P::STAGE;
-  const int TT = P::VT / q;
+  const int TT = VT / q;
   const int64_t ntiles = (T_ + TT - 1) / TT;
   const int64_t tok_elems = (int64_t)q * N;
   auto tile_rows = [&](int64_t t) { return (int)((T_ - t * TT < TT ? T_ - t * TT : TT) * q); };
@@ -85,7 +63,7 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   p2_tables<P>(TWf, TWi, tid, PIPES * NT);
-  for (int pp = 0; pp < PIPES; ++pp) p2_zero_pads<P>(Hbase + (size_t)pp * P::HF, P::VT, tid, PIPES * NT);
+  for (int pp = 0; pp < PIPES; ++pp) p2_zero_pads<P>(Hbase + (size_t)pp * P::HF, VT, tid, PIPES * NT);
   if (tid == 0) {
     for (int pp = 0; pp < PIPES; ++pp) mbar_init(bar - pipe + pp, 1);
     fence_mbar_init();
@@ -95,55 +73,60 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
   __syncthreads();
   tmem_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM address of this thread's item (lane = warp quarter base + lane in warp; 64 columns per item)
-  const int u = lt;
-  const uint32_t taddr = tmem + ((uint32_t)(32 * ((tid / 32) % 4)) << 16) + (uint32_t)(64 * (u / 128));
+  // TMEM address of item u = lt + NT m: lane u % 128 (= this thread's warp-quarter lane), 64 columns
+  // per item at column 64 (u / 128)
+  const uint32_t tlane = tmem + ((uint32_t)(32 * ((tid / 32) % 4)) << 16);
+  auto taddr = [&](int m) { return tlane + (uint32_t)(64 * ((lt + NT * m) / 128)); };
   // ---- first tile of each pipe: start its TMA while W is being transformed
   if (lt == 0) {
     const int64_t t = (int64_t)blockIdx.x * PIPES + pipe;
     if (t < ntiles) stage_issue_rows<P>(x + t * TT * tok_elems, tile_rows(t), stg, bar);
   }
-  // ---- prologue: W_ij = rdFFT(w_ij) into pipe 1's H (scratch), then into TMEM by pipe 0
-  float2* Wtmp = Hbase + (size_t)(PIPES - 1) * P::HF;
+  // ---- prologue (pipe 0): W_ij = rdFFT(w_ij), VT rows at a time, into the H regions of pipes 1..
+  // (scratch), then into TMEM
   if (pipe == 0) {
-    if (wspec) {
-      p2_load_spectra<P>(Wtmp, wspec, q * q, lt, NT);
-      named_bar(1, NT);
-    } else {
-      const P2Roles<P> rw(Wtmp, TWf, TWi, lt);
-      p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
-      named_bar(1, NT);
-      p2_last_fwd<P>(rw, q * q);
-      p2_dc_fwd<P>(rw, q * q);
-      named_bar(1, NT);
-    }
-    int oa, ob;
-    bca_item_offsets<P>(u, oa, ob);
-#pragma unroll
-    for (int g4 = 0; g4 < 4; ++g4) {  // 4 groups of 4 bin pairs = 16 columns each
-      uint32_t r[16];
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        const int c = 4 * g4 + c4;
-        BinPair b = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-        if (c < q * q) b = bins_get(Wtmp + P::row(c), oa, ob, u == 0);
-        r[4 * c4 + 0] = __float_as_uint(b.b1.x);
-        r[4 * c4 + 1] = __float_as_uint(b.b1.y);
-        r[4 * c4 + 2] = __float_as_uint(b.b2.x);
-        r[4 * c4 + 3] = __float_as_uint(b.b2.y);
+    for (int c0 = 0; c0 < q * q; c0 += VT) {
+      float2* Wtmp = Hbase + (size_t)(1 + c0 / VT) * P::HF;
+      const int nr = q * q - c0 < VT ? q * q - c0 : VT;
+      if (wspec) {
+        p2_load_spectra<P>(Wtmp, wspec + (int64_t)c0 * N, nr, lt, NT);
+      } else {
+        const P2Roles<P> rw(Wtmp, TWf, TWi, lt);
+        p2_pass1_fwd<P, true>(rw, w + (int64_t)c0 * N, nr, k65536);
+        named_bar(1, NT);
+        p2_last_fwd<P>(rw, nr);
+        p2_dc_fwd<P>(rw, nr);
       }
-      tmem_st16(taddr + 16 * g4, r);
+    }
+    named_bar(1, NT);
+#pragma unroll
+    for (int m = 0; m < IPT; ++m) {
+      const int u = lt + NT * m;
+      int oa, ob;
+      bca_item_offsets<P>(u, oa, ob);
+#pragma unroll
+      for (int g4 = 0; g4 < 4; ++g4) {  // 4 groups of 4 bin pairs = 16 columns each
+        uint32_t r[16];
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int c = 4 * g4 + c4;
+          BinPair b = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          if (c < q * q) b = bins_get(Hbase + (size_t)(1 + c / VT) * P::HF + P::row(c % VT), oa, ob, u == 0);
+          r[4 * c4 + 0] = __float_as_uint(b.b1.x);
+          r[4 * c4 + 1] = __float_as_uint(b.b1.y);
+          r[4 * c4 + 2] = __float_as_uint(b.b2.x);
+          r[4 * c4 + 3] = __float_as_uint(b.b2.y);
+        }
+        tmem_st16(taddr(m) + 16 * g4, r);
+      }
     }
     tmem_wait_st();
   }
   tmem_fence_before();
-  __syncthreads();  // W in TMEM; pipe 1's H free again (the forward never writes the pads)
+  __syncthreads();  // W in TMEM; the scratch H regions free again (the forward never writes the pads)
   tmem_fence_after();
   const P2Roles<P> rh(H, TWf, TWi, lt);
   const int bid = 1 + pipe;
-  int oa, ob;
-  bca_item_offsets<P>(u, oa, ob);
-  const bool special = (u == 0);
   uint32_t phase = 0;
   for (int64_t tile = (int64_t)blockIdx.x * PIPES + pipe; tile < ntiles; tile += (int64_t)gridDim.x * PIPES) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
@@ -157,13 +140,18 @@ __global__ void __launch_bounds__(PIPES * P::NT, 1) bca_fwd5_kernel(const typena
     p2_last_fwd<P>(rh, nv);
     p2_dc_fwd<P>(rh, nv);
     named_bar(bid, NT);
-    {  // ---- product, W_ij from TMEM
+#pragma unroll 1
+    for (int m = 0; m < IPT; ++m) {  // ---- product, W_ij from TMEM
+      const int u = lt + NT * m;
+      int oa, ob;
+      bca_item_offsets<P>(u, oa, ob);
+      const bool special = (u == 0);
       BinPair wv[Q][Q];
 #pragma unroll
       for (int g4 = 0; g4 < 4; ++g4) {
         if (4 * g4 < q * q) {
           uint32_t r[16];
-          tmem_ld16(taddr + 16 * g4, r);
+          tmem_ld16(taddr(m) + 16 * g4, r);
           tmem_wait_ld(r);
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
@@ -220,12 +208,6 @@ bool launch_bca_fwd5(const typename P::elem* x, const typename P::elem* w, typen
   return true;
 }
 
-#ifndef RDFFT_BCA_FWD_VT
-#define RDFFT_BCA_FWD_VT 16   // p = 1024 forward: 32 vectors (8 tokens of q = 4) per tile, 512 threads
-#endif
-#ifndef RDFFT_BCA_FWD_NSTG
-#define RDFFT_BCA_FWD_NSTG 2  // ... with pass 1 reading x straight from HBM (H + W fill shared memory)
-#endif
 // Fused fast paths: square layers, q <= 4, p in {256, 512, 1024}.  Returns false if none applies.
 template <typename T, int Q>
 bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cudaStream_t st, int acc,
@@ -248,10 +230,11 @@ bool bca_fwd_fast_q(const T* x, const T* w, T* y, int64_t T_, int p, int sms, cu
     case 1024:
       // bf16: W spectra in tensor memory + two staged pipes (bca_fwd5); fp32 keeps the single-pipe
       // kernel (its 8-byte direct loads made the 2-pipe variant slower: 0.194 -> 0.205 ms)
+      // (four pipes of 8 vectors, two product items per thread, measured 0.141 -> 0.146 ms: slower)
       if constexpr (sizeof(T) == 2)
         return launch_bca_fwd5<Plan2<T, 1024, 32, 16>, Q, 2>(x, w, y, T_, sms, st, acc, wspec);
-      return launch_bca_fwd2<Plan2<T, 1024, 32, RDFFT_BCA_FWD_VT, (sizeof(T) == 2 ? RDFFT_BCA_FWD_NSTG : 1)>, Q>(
-          x, w, y, T_, sms, st, acc, wspec);
+      else
+        return launch_bca_fwd2<Plan2<T, 1024, 32, 16, 1>, Q>(x, w, y, T_, sms, st, acc, wspec);
     default: return false;
   }
 }

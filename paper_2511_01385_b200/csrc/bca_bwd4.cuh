@@ -59,7 +59,17 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
   p2_zero_pads<P>(Hg, P::VT, tid, NT2);
   p2_zero_pads<P>(Wr, q * q, tid, NT2);
   const uint32_t k65536 = kTwo16;
+  // dW accumulators in TMEM between tiles (in registers only during the product phase; held across
+  // the transforms they spilled at the 128-register cap): thread t owns lane t % 128, columns
+  // 32 (t / 128) .. + 31, bin pair e = (a QH + c) 2 + r at columns 4 e .. 4 e + 3
+  constexpr uint32_t kCols = 128;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L::TMEM_OFF);
+  tmem_alloc<kCols>(tmem_slot);
+  tmem_fence_before();
   __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tacc = tmem + ((uint32_t)(32 * ((tid / 32) % 4)) << 16) + (uint32_t)(32 * (tid / 128));
   if (wspec) {
     p2_load_spectra<P>(Wr, wspec, q * q, tid, NT2);
   } else if (grp == 0) {  // W_ij = rdFFT(w_ij), q*q <= VT vectors
@@ -82,13 +92,33 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
   const bool special = (u == 0);
   constexpr int QH = (Q + 1) / 2;
   auto jrel = [&](int c, int r) { return 2 * c + (r ? 1 - h : h); };
-  BinPair acc[QH][QH][2];
+  constexpr int NACC = 2 * QH * QH;  // bin pairs per thread (<= 8): one or two 16-column groups
+  {
+    uint32_t z[16];
 #pragma unroll
-  for (int a = 0; a < QH; ++a)
+    for (int k = 0; k < 16; ++k) z[k] = 0u;
+    tmem_st16(tacc, z);
+    if (NACC > 4) tmem_st16(tacc + 16, z);
+    tmem_wait_st();
+  }
+  auto acc_load = [&](BinPair (&acc)[QH][QH][2]) {
+    uint32_t r16[2][16];
+    tmem_ld16(tacc, r16[0]);
+    if (NACC > 4) tmem_ld16(tacc + 16, r16[1]);
+    tmem_wait_ld(r16[0]);
+    if (NACC > 4) tmem_wait_ld(r16[1]);
 #pragma unroll
-    for (int c = 0; c < QH; ++c)
+    for (int a = 0; a < QH; ++a)
 #pragma unroll
-      for (int r = 0; r < 2; ++r) acc[a][c][r] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      for (int c = 0; c < QH; ++c)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int e = (a * QH + c) * 2 + r;
+          const uint32_t* f = &r16[e / 4][4 * (e % 4)];
+          acc[a][c][r] = {make_float2(__uint_as_float(f[0]), __uint_as_float(f[1])),
+                          make_float2(__uint_as_float(f[2]), __uint_as_float(f[3]))};
+        }
+  };
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
     const int nv = ntok * q;
@@ -100,6 +130,8 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
     __syncthreads();
     // ---- products
     {
+      BinPair acc[QH][QH][2];
+      acc_load(acc);
       BinPair wv[QH][QH][2];
 #pragma unroll
       for (int a = 0; a < QH; ++a)
@@ -149,6 +181,23 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
           if (jrel(c, 0) < q) bins_put(Hg + P::row(tt * q + jrel(c, 0)), oa, ob, special, d[0]);
         }
       }
+      uint32_t r16[2][16];
+#pragma unroll
+      for (int a = 0; a < QH; ++a)
+#pragma unroll
+        for (int c = 0; c < QH; ++c)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int e = (a * QH + c) * 2 + r;
+            uint32_t* f = &r16[e / 4][4 * (e % 4)];
+            f[0] = __float_as_uint(acc[a][c][r].b1.x);
+            f[1] = __float_as_uint(acc[a][c][r].b1.y);
+            f[2] = __float_as_uint(acc[a][c][r].b2.x);
+            f[3] = __float_as_uint(acc[a][c][r].b2.y);
+          }
+      tmem_st16(tacc, r16[0]);
+      if (NACC > 4) tmem_st16(tacc + 16, r16[1]);
+      tmem_wait_st();
     }
     __syncthreads();  // D complete in Hg; Hx free
     if (grp == 0) {
@@ -162,6 +211,8 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
     }
   }
   // ---- flush dW accumulators into dw (packed slots) with fp32 atomics
+  BinPair acc[QH][QH][2];
+  acc_load(acc);
 #pragma unroll
   for (int a = 0; a < QH; ++a)
 #pragma unroll
@@ -185,6 +236,10 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd4_kernel(const typename P
         }
       }
     }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  tmem_free<kCols>(tmem);
 }
 
 template <typename P, int Q>

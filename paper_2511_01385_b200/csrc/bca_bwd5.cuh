@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
   constexpr int N = P::N, NT = P::NT, NT2 = 2 * NT, NI = N / 4;
   static_assert(Q * Q <= P::VT && Q % 2 == 0, "even q; the W prologue runs on one group");
   static_assert(NT2 == 2 * NI && NI == 256, "one thread pair per item, four threads per TMEM lane");
-  constexpr uint32_t kCols = 128;
+  // columns 0 .. 127: W (32 per m = t / 128); 128 .. 255: this thread's dW accumulators (32 per m)
+  constexpr uint32_t kCols = 256;
   enum { kBarG0 = 1, kBarG1 = 2, kBarLI = 3 };
   extern __shared__ float4 smem4[];
   unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
       for (int c = 0; c < QH; ++c)
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-          const int e = (a * QH + c) * 2 + r;  // bin pair index 0 .. 2 QH^2 - 1 (<= 7)
+          const int e = (c * QH + a) * 2 + r;  // bin pair index 0 .. 2 QH^2 - 1 (<= 7): c-major
           const BinPair b = bins_get(Hg + P::row((2 * a + h) * q + jrel(c, r)), oa, ob, special);
           r16[e / 4][4 * (e % 4) + 0] = __float_as_uint(b.b1.x);
           r16[e / 4][4 * (e % 4) + 1] = __float_as_uint(b.b1.y);
@@ -120,13 +121,19 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
   tmem_fence_after();
   const P2Roles<P> rm(grp ? Hg : Hx, TWf, TWi, lt);
   const P2Roles<P> rd(Hg, TWf, TWi, lt);
-  BinPair acc[QH][QH][2];
+  // dW accumulators (2 QH^2 bin pairs per thread) live in TMEM between tiles and in registers only
+  // during the product phase: held in registers across the transforms they spilled at the
+  // 128-register cap.  Layout as W's (pair e = (c QH + a) 2 + r), 128 columns further.
+  const uint32_t tacc = taddr + 128;
+  constexpr int NACC = 2 * QH * QH;  // bin pairs (<= 8): one or two 16-column groups
+  {
+    uint32_t z[16];
 #pragma unroll
-  for (int a = 0; a < QH; ++a)
-#pragma unroll
-    for (int c = 0; c < QH; ++c)
-#pragma unroll
-      for (int r = 0; r < 2; ++r) acc[a][c][r] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    for (int k = 0; k < 16; ++k) z[k] = 0u;
+    tmem_st16(tacc, z);
+    if (NACC > 4) tmem_st16(tacc + 16, z);
+    tmem_wait_st();
+  }
   uint32_t phase = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
@@ -140,62 +147,93 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
     p2_last_fwd<P>(rm, nv);
     p2_dc_fwd<P>(rm, nv);
     __syncthreads();
-    {  // ---- products (W from TMEM)
-      BinPair wv[QH][QH][2];
-      {
-        uint32_t r16[2][16];
-        tmem_ld16(taddr, r16[0]);
-        if (2 * QH * QH > 4) tmem_ld16(taddr + 16, r16[1]);
-        tmem_wait_ld(r16[0]);
-        if (2 * QH * QH > 4) tmem_wait_ld(r16[1]);
+    // ---- products (W from TMEM, c-major layout: the 2 QH bin pairs of input-block pair c are one
+    // 16-column group, loaded per (token, c), so only a quarter of W is live in registers at a time;
+    // holding all of W across the token loop spilled 20 B at the 128-register cap)
+    BinPair acc[QH][QH][2];
+    {
+      uint32_t r16[2][16];
+      tmem_ld16(tacc, r16[0]);
+      if (NACC > 4) tmem_ld16(tacc + 16, r16[1]);
+      tmem_wait_ld(r16[0]);
+      if (NACC > 4) tmem_wait_ld(r16[1]);
 #pragma unroll
-        for (int a = 0; a < QH; ++a)
-#pragma unroll
-          for (int c = 0; c < QH; ++c)
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int e = (a * QH + c) * 2 + r;
-              wv[a][c][r] = {make_float2(__uint_as_float(r16[e / 4][4 * (e % 4)]),
-                                         __uint_as_float(r16[e / 4][4 * (e % 4) + 1])),
-                             make_float2(__uint_as_float(r16[e / 4][4 * (e % 4) + 2]),
-                                         __uint_as_float(r16[e / 4][4 * (e % 4) + 3]))};
-            }
-      }
-      for (int tt = 0; tt < ntok; ++tt) {
-        BinPair xv[QH][2];
-        float2 g2[QH];
-        PrepB g1[QH];
+      for (int a = 0; a < QH; ++a)
 #pragma unroll
         for (int c = 0; c < QH; ++c)
 #pragma unroll
-          for (int r = 0; r < 2; ++r) xv[c][r] = bins_get(Hx + P::row(tt * q + jrel(c, r)), oa, ob, special);
+          for (int r = 0; r < 2; ++r) {
+            const int e = (c * QH + a) * 2 + r;
+            const uint32_t* f = &r16[e / 4][4 * (e % 4)];
+            acc[a][c][r] = {make_float2(__uint_as_float(f[0]), __uint_as_float(f[1])),
+                            make_float2(__uint_as_float(f[2]), __uint_as_float(f[3]))};
+          }
+    }
+    for (int tt = 0; tt < ntok; ++tt) {
+      float2 g2[QH];
+      PrepB g1[QH];
 #pragma unroll
-        for (int a = 0; a < QH; ++a) {
-          const BinPair gb = bins_get(Hg + P::row(tt * q + 2 * a + h), oa, ob, special);
-          g1[a] = prep_b<true>(gb.b1, special);
-          g2[a] = gb.b2;
+      for (int a = 0; a < QH; ++a) {
+        const BinPair gb = bins_get(Hg + P::row(tt * q + 2 * a + h), oa, ob, special);
+        g1[a] = prep_b<true>(gb.b1, special);
+        g2[a] = gb.b2;
+      }
+#pragma unroll
+      for (int c = 0; c < QH; ++c) {
+        BinPair wv[QH][2];
+        {
+          uint32_t r16[16];
+          tmem_ld16(taddr + 16 * (2 * QH * c / 4), r16);
+          tmem_wait_ld(r16);
+#pragma unroll
+          for (int a = 0; a < QH; ++a)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const int e = (2 * QH * c + 2 * a + r) % 4;  // position inside the 4-pair group
+              wv[a][r] = {make_float2(__uint_as_float(r16[4 * e]), __uint_as_float(r16[4 * e + 1])),
+                          make_float2(__uint_as_float(r16[4 * e + 2]), __uint_as_float(r16[4 * e + 3]))};
+            }
         }
+        BinPair xv[2];
 #pragma unroll
-        for (int c = 0; c < QH; ++c) {
-          BinPair d[2];
+        for (int r = 0; r < 2; ++r) xv[r] = bins_get(Hx + P::row(tt * q + jrel(c, r)), oa, ob, special);
+        BinPair d[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          d[r] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int a = 0; a < QH; ++a) {
+            acc[a][c][r].b1 = pmac(xv[r].b1, g1[a], acc[a][c][r].b1);
+            acc[a][c][r].b2 = cfmac(xv[r].b2, g2[a], acc[a][c][r].b2);
+            d[r].b1 = pmac(wv[a][r].b1, g1[a], d[r].b1);
+            d[r].b2 = cfmac(wv[a][r].b2, g2[a], d[r].b2);
+          }
+        }
+        d[0].b1.x += __shfl_xor_sync(0xffffffffu, d[1].b1.x, 1);
+        d[0].b1.y += __shfl_xor_sync(0xffffffffu, d[1].b1.y, 1);
+        d[0].b2.x += __shfl_xor_sync(0xffffffffu, d[1].b2.x, 1);
+        d[0].b2.y += __shfl_xor_sync(0xffffffffu, d[1].b2.y, 1);
+        bins_put(Hg + P::row(tt * q + jrel(c, 0)), oa, ob, special, d[0]);
+      }
+    }
+    {
+      uint32_t r16[2][16];
+#pragma unroll
+      for (int a = 0; a < QH; ++a)
+#pragma unroll
+        for (int c = 0; c < QH; ++c)
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
-            d[r] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-            for (int a = 0; a < QH; ++a) {
-              acc[a][c][r].b1 = pmac(xv[c][r].b1, g1[a], acc[a][c][r].b1);
-              acc[a][c][r].b2 = cfmac(xv[c][r].b2, g2[a], acc[a][c][r].b2);
-              d[r].b1 = pmac(wv[a][c][r].b1, g1[a], d[r].b1);
-              d[r].b2 = cfmac(wv[a][c][r].b2, g2[a], d[r].b2);
-            }
+            const int e = (c * QH + a) * 2 + r;
+            uint32_t* f = &r16[e / 4][4 * (e % 4)];
+            f[0] = __float_as_uint(acc[a][c][r].b1.x);
+            f[1] = __float_as_uint(acc[a][c][r].b1.y);
+            f[2] = __float_as_uint(acc[a][c][r].b2.x);
+            f[3] = __float_as_uint(acc[a][c][r].b2.y);
           }
-          d[0].b1.x += __shfl_xor_sync(0xffffffffu, d[1].b1.x, 1);
-          d[0].b1.y += __shfl_xor_sync(0xffffffffu, d[1].b1.y, 1);
-          d[0].b2.x += __shfl_xor_sync(0xffffffffu, d[1].b2.x, 1);
-          d[0].b2.y += __shfl_xor_sync(0xffffffffu, d[1].b2.y, 1);
-          bins_put(Hg + P::row(tt * q + jrel(c, 0)), oa, ob, special, d[0]);
-        }
-      }
+      tmem_st16(tacc, r16[0]);
+      if (NACC > 4) tmem_st16(tacc + 16, r16[1]);
+      tmem_wait_st();
     }
     __syncthreads();  // D complete in Hg; Hx free
     if (grp == 0) {
@@ -208,6 +246,11 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
       named_bar(kBarG1, NT);  // Hg free for the next tile's g
     }
   }
+  uint32_t fin[2][16];
+  tmem_ld16(tacc, fin[0]);
+  if (NACC > 4) tmem_ld16(tacc + 16, fin[1]);
+  tmem_wait_ld(fin[0]);
+  if (NACC > 4) tmem_wait_ld(fin[1]);
   // ---- flush dW accumulators into dw (packed slots) with fp32 atomics
 #pragma unroll
   for (int a = 0; a < QH; ++a)
@@ -217,7 +260,10 @@ __global__ void __launch_bounds__(2 * P::NT, 1) bca_bwd5_kernel(const typename P
       for (int r = 0; r < 2; ++r) {
         const int i = 2 * a + h, j = jrel(c, r);
         float* d = dw + (int64_t)(i * q + j) * N;
-        const BinPair v = acc[a][c][r];
+        const int e = (c * QH + a) * 2 + r;
+        const uint32_t* f = &fin[e / 4][4 * (e % 4)];
+        const BinPair v = {make_float2(__uint_as_float(f[0]), __uint_as_float(f[1])),
+                           make_float2(__uint_as_float(f[2]), __uint_as_float(f[3]))};
         if (special) {
           atomicAdd(d + 0, v.b1.x);
           atomicAdd(d + N / 2, v.b1.y);

@@ -46,10 +46,10 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_fwd_tiled_kernel(const T
   const int hb = p >> 1;
   const int64_t d_in = (int64_t)q_in * p, d_out = (int64_t)q_out * p;
   const int i0 = blockIdx.y * grp, i1 = min(q_out, i0 + grp);
-  const int64_t ntiles = (T_ + vt - 1) / vt;
+  const int ntiles = (int)((T_ + vt - 1) / vt);  // 32-bit tile indices (T < 2^31 tokens)
   __syncthreads();
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t t0 = tile * vt;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t t0 = (int64_t)tile * vt;
     const int nv = (int)(T_ - t0 < vt ? T_ - t0 : vt);
     load_rows<T>(x + t0 * d_in, X, nv * q_in * p, p, logp, /*rev=*/true);
     __syncthreads();
@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(kBcaTiledThreads) bca_fwd_tiled_kernel(const T
         fwd_stages_smem(Wr, q_in, p, logp, tw);
       }
       for (int it = threadIdx.x; it < nv * hb; it += blockDim.x) {
-        const int v = it / hb;
-        const PackedBin bin{p, it - v * hb};
+        const int v = it >> (logp - 1);  // hb = p / 2 is a power of two: no integer division
+        const PackedBin bin{p, it & (hb - 1)};
         float2 acc = make_float2(0.f, 0.f);
         for (int j = 0; j < q_in; ++j) {
           const float2 prod = bin.mul(bin.get(Wr + (size_t)j * p), bin.get(X + ((size_t)v * q_in + j) * p));

@@ -236,7 +236,7 @@ __device__ __forceinline__ void p2_zero_pads(float2* H, int nvec, int tid, int n
 // pass 1 from a staged tile (shared memory, natural order, element type T)
 template <typename P, bool kGlobal = false>
 __device__ __forceinline__ void p2_pass1_fwd(const P2Roles<P>& r, const typename P::elem* st, int nv,
-                                             uint32_t k65536) {
+                                             uint32_t k65536, int hoff = 0) {
   using T = typename P::elem;
   constexpr int R = P::R, S = P::S;
   if (r.act1 && r.v1 < nv) {
@@ -252,20 +252,20 @@ __device__ __forceinline__ void p2_pass1_fwd(const P2Roles<P>& r, const typename
     rfft_fwd_reg<R>(b);
     ct::static_for<0, R / 2>([&](auto I) {
       constexpr int i = 2 * decltype(I)::value;
-      *reinterpret_cast<float4*>(r.h1 + i) = make_float4(b[i].x, b[i].y, b[i + 1].x, b[i + 1].y);
+      *reinterpret_cast<float4*>(r.h1 + hoff + i) = make_float4(b[i].x, b[i].y, b[i + 1].x, b[i + 1].y);
     });
   }
 }
 
 template <typename P>
-__device__ __forceinline__ void p2_last_fwd(const P2Roles<P>& r, int nv) {
+__device__ __forceinline__ void p2_last_fwd(const P2Roles<P>& r, int nv, int hoff = 0) {
   constexpr int M = P::M, WSTR = P::WSTR;
   if (r.v2 < nv) {
     float zr[M], zi[M];
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
-      const float2 a = r.ha[jj * WSTR];
-      const float2 bb = r.hmz[jj * WSTR];
+      const float2 a = r.ha[hoff + jj * WSTR];
+      const float2 bb = r.hmz[hoff + jj * WSTR];
       zr[jj] = a.x;
       zr[jj + M / 2] = a.y;
       zi[jj] = bb.x;
@@ -286,27 +286,27 @@ __device__ __forceinline__ void p2_last_fwd(const P2Roles<P>& r, int nv) {
     cfft_dit<M>(zr, zi);
     ct::static_for<0, M / 2>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
-      r.ha[q * WSTR] = make_float2(zr[q], -zi[q + M / 2]);
-      r.hm[(M / 2 - 1 - q) * WSTR] = make_float2(zr[q + M / 2], zi[q]);
+      r.ha[hoff + q * WSTR] = make_float2(zr[q], -zi[q + M / 2]);
+      r.hm[hoff + (M / 2 - 1 - q) * WSTR] = make_float2(zr[q + M / 2], zi[q]);
     });
   }
 }
 
 template <typename P>
-__device__ __forceinline__ void p2_dc_fwd(const P2Roles<P>& r, int nv) {
+__device__ __forceinline__ void p2_dc_fwd(const P2Roles<P>& r, int nv, int hoff = 0) {
   constexpr int M = P::M, WSTR = P::WSTR;
   if (r.dv >= 0 && r.dv < nv) {  // block DCs j R: packed real M-point DFT (input already bit-reversed)
     float d[M];
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
-      const float2 a = r.hd[jj * WSTR];
+      const float2 a = r.hd[hoff + jj * WSTR];
       d[jj] = a.x;
       d[jj + M / 2] = a.y;
     });
     rfft_fwd_reg<M>(d);
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
-      r.hd[jj * WSTR] = make_float2(d[jj], d[jj + M / 2]);
+      r.hd[hoff + jj * WSTR] = make_float2(d[jj], d[jj + M / 2]);
     });
   }
 }
@@ -439,7 +439,7 @@ __device__ __forceinline__ void p2_load(const P2Roles<P>& r, const typename P::e
 }
 
 template <typename P>
-__device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv) {
+__device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv, int hoff = 0) {
   constexpr int M = P::M, WSTR = P::WSTR, LM = P::LM;
   if (r.v2 < nv) {
     // Y[q] is loaded into register rev(q); a DIT pass with conjugate twiddles then leaves
@@ -447,8 +447,8 @@ __device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv) {
     float zr[M], zi[M];
     ct::static_for<0, M / 2>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
-      const float2 a = r.ha[q * WSTR];                    // (Re Y[q], -Im Y[q + M/2])
-      const float2 bb = r.hm[(M / 2 - 1 - q) * WSTR];     // (Re Y[q + M/2], Im Y[q])
+      const float2 a = r.ha[hoff + q * WSTR];                    // (Re Y[q], -Im Y[q + M/2])
+      const float2 bb = r.hm[hoff + (M / 2 - 1 - q) * WSTR];     // (Re Y[q + M/2], Im Y[q])
       zr[rev_bits<LM>(q)] = a.x;
       zi[rev_bits<LM>(q + M / 2)] = -a.y;
       zr[rev_bits<LM>(q + M / 2)] = bb.x;
@@ -469,29 +469,29 @@ __device__ __forceinline__ void p2_last_inv(const P2Roles<P>& r, int nv) {
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
       constexpr int r1 = rev_bits<LM>(jj), r2 = rev_bits<LM>(jj + M / 2);
-      r.ha[jj * WSTR] = make_float2(zr[r1], zr[r2]);
+      r.ha[hoff + jj * WSTR] = make_float2(zr[r1], zr[r2]);
       // k = R/2: the imaginary part (zero up to rounding) is dropped, so the pad keeps the exact
       // zero the next forward pass of the same buffer reads (fused BCA kernels reuse H per tile)
-      if (!r.kz) r.hm[jj * WSTR] = make_float2(zi[r1], zi[r2]);
+      if (!r.kz) r.hm[hoff + jj * WSTR] = make_float2(zi[r1], zi[r2]);
     });
   }
 }
 
 template <typename P>
-__device__ __forceinline__ void p2_dc_inv(const P2Roles<P>& r, int nv) {
+__device__ __forceinline__ void p2_dc_inv(const P2Roles<P>& r, int nv, int hoff = 0) {
   constexpr int M = P::M, WSTR = P::WSTR;
   if (r.dv >= 0 && r.dv < nv) {
     float d[M];
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
-      const float2 a = r.hd[jj * WSTR];
+      const float2 a = r.hd[hoff + jj * WSTR];
       d[jj] = a.x;
       d[jj + M / 2] = a.y;
     });
     rfft_inv_reg<M>(d);
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
-      r.hd[jj * WSTR] = make_float2(d[jj] * (1.0f / P::N), d[jj + M / 2] * (1.0f / P::N));
+      r.hd[hoff + jj * WSTR] = make_float2(d[jj] * (1.0f / P::N), d[jj + M / 2] * (1.0f / P::N));
     });
   }
 }
@@ -500,14 +500,14 @@ __device__ __forceinline__ void p2_dc_inv(const P2Roles<P>& r, int nv) {
 // acc: dst += result (the BCA forward's y += BCA(x) mode) instead of dst = result
 template <typename P>
 __device__ __forceinline__ void p2_pass1_inv(const P2Roles<P>& r, typename P::elem* dst_tile, int nv,
-                                             bool acc = false) {
+                                             bool acc = false, int hoff = 0) {
   using T = typename P::elem;
   constexpr int R = P::R, S = P::S;
   if (r.act1 && r.v1 < nv) {
     float2 b[R];
     ct::static_for<0, R / 2>([&](auto I) {
       constexpr int i = 2 * decltype(I)::value;
-      const float4 f = *reinterpret_cast<const float4*>(r.h1 + i);
+      const float4 f = *reinterpret_cast<const float4*>(r.h1 + hoff + i);
       b[i] = make_float2(f.x, f.y);
       b[i + 1] = make_float2(f.z, f.w);
     });

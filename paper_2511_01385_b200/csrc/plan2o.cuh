@@ -108,29 +108,31 @@ __global__ void __launch_bounds__(P::NTT, 4) rdfft2o_inv_kernel(__nv_bfloat16* _
   }
   const P2Roles<P> r(H, TW, TW, tid);
   const uint32_t k65536 = kTwo16;
-  const int64_t ntiles = (batch + VT - 1) / VT;
-  auto tile_rows = [&](int64_t t) { return (int)(batch - t * VT < VT ? batch - t * VT : VT); };
+  // 32-bit tile indices (bf16 rows of n >= 128 elements: < 2^31 tiles in any device memory) keep
+  // the loop state small enough for the 96-register cap of 4 CTAs/SM without spilling
+  const int ntiles = (int)((batch + VT - 1) / VT);
+  auto tile_rows = [&](int t) { return (int)(batch - (int64_t)t * VT < VT ? batch - (int64_t)t * VT : VT); };
   __syncthreads();
   if (tid == 0) {
     for (int q = 0; q < NS; ++q) {
-      const int64_t t = blockIdx.x + (int64_t)q * gridDim.x;
-      if (t < ntiles) stage_issue_rows<P>(x + t * VT * (int64_t)N, tile_rows(t), base + q * P::STAGE, bar + q);
+      const int t = (int)blockIdx.x + q * (int)gridDim.x;
+      if (t < ntiles) stage_issue_rows<P>(x + (int64_t)t * VT * N, tile_rows(t), base + q * P::STAGE, bar + q);
     }
   }
   const bool dcw = tid >= P::DC0;
   int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int nv = tile_rows(tile);
-    T* xt = x + tile * VT * (int64_t)N;
+    T* xt = x + (int64_t)tile * VT * N;
     const int sb = it % NS;
     const T* st = reinterpret_cast<const T*>(base + sb * P::STAGE);
-    const int64_t nxt = tile + NS * (int64_t)gridDim.x;
+    const int nxt = tile + NS * (int)gridDim.x;
     mbar_wait(bar + sb, (it / NS) & 1);
     if (!dcw) p2o_last_inv<P>(r, st, nv, k65536);
     else p2o_dc_inv<P>(r, st, nv, k65536);
     __syncthreads();  // H complete; staging buffer consumed
     if (tid == 0 && nxt < ntiles)
-      stage_issue_rows<P>(x + nxt * VT * (int64_t)N, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
+      stage_issue_rows<P>(x + (int64_t)nxt * VT * N, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
     p2_pass1_inv<P>(r, xt, nv);
     __syncthreads();  // H free for the next tile
   }
