@@ -311,9 +311,26 @@ __device__ __forceinline__ void p2_dc_fwd(const P2Roles<P>& r, int nv, int hoff 
   }
 }
 
-// Forward last pass / DC set writing the packed outputs straight to the global tile (P::FD):
-// the slots p2_last_fwd / p2_dc_fwd would write into H, in natural order.
-template <typename P>
+// Single-element shared-memory stores of T (output staging tile), narrowed with RNE.
+template <typename T>
+struct sst1;
+template <>
+struct sst1<float> {
+  __device__ __forceinline__ static void st1(float* p, float v) { *p = v; }
+  __device__ __forceinline__ static void st2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+};
+template <>
+struct sst1<__nv_bfloat16> {
+  __device__ __forceinline__ static void st1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+  __device__ __forceinline__ static void st2(__nv_bfloat16* p, float2 v) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v.x, v.y);
+  }
+};
+
+// Forward last pass / DC set writing the packed outputs straight to the global tile (P::FD) or,
+// with ST = sst1<T> and RS = the staged row stride, into an output staging tile: the slots
+// p2_last_fwd / p2_dc_fwd would write into H, in natural order.
+template <typename P, typename ST = gio<typename P::elem>, int RS = P::N>
 __device__ __forceinline__ void p2_last_fwd_direct(const P2Roles<P>& r, typename P::elem* dst, int nv) {
   using T = typename P::elem;
   constexpr int M = P::M, WSTR = P::WSTR, R = P::R, N = P::N;
@@ -341,21 +358,21 @@ __device__ __forceinline__ void p2_last_fwd_direct(const P2Roles<P>& r, typename
       zi[j0 + 1] = fmaf(q1, t2.w, zi[j0 + 1] * t2.z);
     });
     cfft_dit<M>(zr, zi);
-    T* da = dst + r.v2 * N + r.k;        // slots q R + k (and + N/2)
-    T* dm = dst + r.v2 * N + (R - r.k);  // slots q R + R - k
+    T* da = dst + r.v2 * RS + r.k;        // slots q R + k (and + N/2)
+    T* dm = dst + r.v2 * RS + (R - r.k);  // slots q R + R - k
     ct::static_for<0, M / 2>([&](auto Q) {
       constexpr int q = decltype(Q)::value;
-      gio<T>::st1(da + q * R, zr[q]);
-      gio<T>::st1(da + q * R + N / 2, -zi[q + M / 2]);
+      ST::st1(da + q * R, zr[q]);
+      ST::st1(da + q * R + N / 2, -zi[q + M / 2]);
       if (!r.kz) {  // k = R/2: the mirror slot is the same slot (written from the ascending side)
-        gio<T>::st1(dm + (M / 2 - 1 - q) * R, zr[q + M / 2]);
-        gio<T>::st1(dm + (M / 2 - 1 - q) * R + N / 2, zi[q]);
+        ST::st1(dm + (M / 2 - 1 - q) * R, zr[q + M / 2]);
+        ST::st1(dm + (M / 2 - 1 - q) * R + N / 2, zi[q]);
       }
     });
   }
 }
 
-template <typename P>
+template <typename P, typename ST = gio<typename P::elem>, int RS = P::N>
 __device__ __forceinline__ void p2_dc_fwd_direct(const P2Roles<P>& r, typename P::elem* dst, int nv) {
   using T = typename P::elem;
   constexpr int M = P::M, WSTR = P::WSTR, R = P::R, N = P::N;
@@ -368,11 +385,11 @@ __device__ __forceinline__ void p2_dc_fwd_direct(const P2Roles<P>& r, typename P
       d[jj + M / 2] = a.y;
     });
     rfft_fwd_reg<M>(d);
-    T* dd = dst + r.dv * N;
+    T* dd = dst + r.dv * RS;
     ct::static_for<0, M / 2>([&](auto J) {
       constexpr int jj = decltype(J)::value;
-      gio<T>::st1(dd + jj * R, d[jj]);
-      gio<T>::st1(dd + jj * R + N / 2, d[jj + M / 2]);
+      ST::st1(dd + jj * R, d[jj]);
+      ST::st1(dd + jj * R + N / 2, d[jj + M / 2]);
     });
   }
 }
@@ -651,6 +668,105 @@ bool launch_plan2_dir(typename P::elem* x, int64_t batch, int sms, cudaStream_t 
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
   k<<<grid, P::NTT, L::BYTES, st>>>(x, batch);
+  return true;
+}
+
+// ---------------------------------------------------------------- forward with an output tile
+// The last pass and the DC lanes write the packed outputs (element type T, RNE for bf16) into an
+// output staging tile O in natural order; one thread then stores O's rows with TMA bulk copies
+// (cp.async.bulk shared -> global).  Against rdfft2_kernel this drops the H -> HBM store phase
+// (a fp32 read of H per element plus the STG instructions) for one narrow shared store per element,
+// and the outputs reach HBM as whole contiguous rows.  O is reused per tile once the previous
+// tile's bulk store has read it (cp.async.bulk.wait_group.read before the barrier that precedes
+// the last pass).  NSTG = 0: pass 1 reads HBM directly (no input staging buffer).
+// O row skew (bytes, 16-byte multiples for the bulk copies): the two interleaved vectors of an
+// R = 32 warp (16 lanes x 2 B each) fall on disjoint banks and the 8 DC lanes (one per vector) on 8
+// distinct banks at a stride of 20 words (bf16); R = 16 (4 vectors of 8 lanes per warp) uses 12
+// words; fp32 rows are 16 lanes x 4 B, so 16 words.
+template <typename P>
+struct P2fSmem {
+  using T = typename P::elem;
+  static constexpr int OSKEWB = sizeof(T) == 2 ? (P::R == 32 ? 80 : 48) : (P::R == 32 ? 64 : 32);
+  static constexpr int OROW = P::N + OSKEWB / (int)sizeof(T);
+  static constexpr size_t O_OFF = (size_t)P::NSTG * P::STAGE;
+  static constexpr size_t H_OFF = O_OFF + (size_t)P::VT * OROW * sizeof(T);
+  static constexpr size_t TW_OFF = H_OFF + (size_t)P::HF * 8;
+  static constexpr size_t BAR_OFF = TW_OFF + (size_t)P::TWF * 8;
+  static constexpr size_t BYTES = BAR_OFF + 8 * (P::NSTG > 0 ? P::NSTG : 1);
+  static_assert((OROW * sizeof(T)) % 16 == 0 && O_OFF % 16 == 0, "O rows must be 16-byte aligned (bulk copies)");
+};
+
+template <typename P>
+__global__ void __launch_bounds__(P::NT) rdfft2fo_kernel(typename P::elem* __restrict__ x, int64_t batch) {
+  using T = typename P::elem;
+  using L = P2fSmem<P>;
+  constexpr int VT = P::VT, N = P::N, NS = P::NSTG;
+  static_assert(NS <= 1, "one input staging buffer (or none)");
+  extern __shared__ float4 smem4[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
+  T* O = reinterpret_cast<T*>(base + L::O_OFF);
+  float2* H = reinterpret_cast<float2*>(base + L::H_OFF);
+  float2* TW = reinterpret_cast<float2*>(base + L::TW_OFF);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
+  const int tid = threadIdx.x;
+  p2_tables<P>(TW, nullptr, tid, P::NT);
+  p2_zero_pads<P>(H, VT, tid, P::NT);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  const P2Roles<P> r(H, TW, TW, tid);
+  const uint32_t k65536 = kTwo16;
+  const int64_t ntiles = (batch + VT - 1) / VT;
+  auto tile_rows = [&](int64_t t) { return (int)(batch - t * VT < VT ? batch - t * VT : VT); };
+  __syncthreads();
+  if (NS > 0 && tid == 0 && (int64_t)blockIdx.x < ntiles)
+    stage_issue_rows<P>(x + (int64_t)blockIdx.x * VT * N, tile_rows(blockIdx.x), base, bar);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int nv = tile_rows(tile);
+    T* xt = x + tile * VT * (int64_t)N;
+    if constexpr (NS > 0) {
+      mbar_wait(bar, it & 1);
+      p2_pass1_fwd<P>(r, reinterpret_cast<const T*>(base), nv, k65536);
+    } else {
+      p2_pass1_fwd<P, true>(r, xt, nv, k65536);
+    }
+    if (tid == 0) bulk_wait_read<0>();  // the previous tile's bulk store has read O
+    __syncthreads();                    // H complete; staging buffer consumed; O free
+    const int64_t nxt = tile + gridDim.x;
+    if (NS > 0 && tid == 0 && nxt < ntiles) stage_issue_rows<P>(x + nxt * VT * (int64_t)N, tile_rows(nxt), base, bar);
+    p2_last_fwd_direct<P, sst1<T>, L::OROW>(r, O, nv);
+    p2_dc_fwd_direct<P, sst1<T>, L::OROW>(r, O, nv);
+    fence_proxy_async_smem();  // O's generic-proxy writes before the bulk store reads them
+    __syncthreads();           // O complete; H free for the next tile
+    if (tid == 0) {
+      for (int v = 0; v < nv; ++v) bulk_s2g(xt + (int64_t)v * N, O + v * L::OROW, (uint32_t)(N * sizeof(T)));
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait<0>();
+}
+
+template <typename P>
+bool launch_plan2fo(typename P::elem* x, int64_t batch, int sms, cudaStream_t st) {
+  using L = P2fSmem<P>;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
+  auto k = rdfft2fo_kernel<P>;
+  static int per_sm_dev[kMaxDevices] = {};
+  int& per_sm = per_sm_dev[device_index()];
+  if (!per_sm) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NT, L::BYTES);
+    if (per_sm < 1) per_sm = 1;
+    if (verbose())
+      std::fprintf(stderr, "[rdfft] plan2fo n=%d R=%d VT=%d NSTG=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N, P::R,
+                   P::VT, P::NSTG, (size_t)L::BYTES, P::NT, per_sm);
+  }
+  const int64_t tiles = (batch + P::VT - 1) / P::VT;
+  const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
+  k<<<grid, P::NT, L::BYTES, st>>>(x, batch);
   return true;
 }
 
