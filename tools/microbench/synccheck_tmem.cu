@@ -6,6 +6,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o /tmp/sct synccheck_tmem.cu
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -45,14 +46,13 @@ __global__ void __launch_bounds__(256, 1) k(float* out) {
   if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(slot) : "memory");
 }
 
-int main() {
+int main(int argc, char** argv) {  // argv[1]: the mode to run (one per process: a failure is sticky)
+  const int mode = argc > 1 ? atoi(argv[1]) : 0;
   float* out;
   cudaMalloc(&out, 4 * 256 * 4);
-  k<0><<<4, 256>>>(out);
-  printf("mode 0: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
-  k<1><<<4, 256>>>(out);
-  printf("mode 1: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
-  k<2><<<4, 256>>>(out);
-  printf("mode 2: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  if (mode == 0) k<0><<<4, 256>>>(out);
+  if (mode == 1) k<1><<<4, 256>>>(out);
+  if (mode == 2) k<2><<<4, 256>>>(out);
+  printf("mode %d: %s\n", mode, cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
