@@ -20,18 +20,15 @@
 #include "plan2o.cuh"
 #include "small.cuh"
 #include "planl.cuh"
+#include "plan2s.cuh"
 
 namespace rdfft {
 
-template <typename T, int N_, int VT_, int NSTG_ = 2, bool FD_ = false, bool O_ = false>
+template <typename T, int N_, int VT_, int NSTG_ = 2, bool FD_ = false>
 struct Plan3 {
   using elem = T;
   static constexpr int N = N_, VT = VT_, R = 32, NSTG = NSTG_;
   static constexpr bool FD = FD_;  // forward last pass stores straight to HBM (see Plan2::FD)
-  // O: the forward's last pass (FD's slots) and the inverse's pass 1 write an output staging tile
-  // that one thread stores with TMA bulk copies (plan2's rdfft2fo_kernel scheme)
-  static constexpr bool O = O_;
-  static constexpr int OROW = O_ ? N_ + 16 / (int)sizeof(T) : 0;  // 16-byte skew: DC lanes of 2 rows
   static constexpr int M2 = 4, W2 = 128;     // middle pass
   static constexpr int M3 = N / W2, LM3 = ilog2c<M3>();
   static constexpr int LR = 5, S = N / R, LS = ilog2c<S>(), P1 = S / 2;
@@ -60,9 +57,8 @@ struct Plan3 {
 };
 
 template <typename P>
-struct P3Smem {  // [stage 0][stage 1][O][H][TWm][TWl][bars]
-  static constexpr size_t O_OFF = (size_t)P::NSTG * P::STAGE;
-  static constexpr size_t H_OFF = O_OFF + (size_t)P::VT * P::OROW * sizeof(typename P::elem);
+struct P3Smem {  // [stage 0][stage 1][H][TWm][TWl][bars]
+  static constexpr size_t H_OFF = (size_t)P::NSTG * P::STAGE;
   static constexpr size_t TWM_OFF = H_OFF + (size_t)P::HF * 8;
   static constexpr size_t TWL_OFF = TWM_OFF + (size_t)P::TWM * 8;
   static constexpr size_t BAR_OFF = TWL_OFF + (size_t)P::TWL * 8;
@@ -209,7 +205,7 @@ __device__ __forceinline__ void p3_last_set(float2* ha, float2* hm, const float2
 
 // Forward last-pass set storing its packed outputs straight to the global row (Plan3::FD):
 // da -> slot k of the row, dm -> slot 128 - k; kz: k = 64, whose mirror slot is its own.
-template <int M, typename T, typename ST = gio<T>>
+template <int M, typename T>
 __device__ __forceinline__ void p3_last_set_fwd_direct(const float2* ha, const float2* hmi, const LTw& tw, T* da,
                                                        T* dm, bool kz, int n) {
   constexpr int WS = 4 * 34, LM = ilog2c<M>();
@@ -230,17 +226,17 @@ __device__ __forceinline__ void p3_last_set_fwd_direct(const float2* ha, const f
   cfft_dit<M>(zr, zi);
   ct::static_for<0, M / 2>([&](auto Q) {
     constexpr int q = decltype(Q)::value;
-    ST::st1(da + q * 128, zr[q]);
-    ST::st1(da + q * 128 + n / 2, -zi[q + M / 2]);
+    gio<T>::st1(da + q * 128, zr[q]);
+    gio<T>::st1(da + q * 128 + n / 2, -zi[q + M / 2]);
     if (!kz) {
-      ST::st1(dm + (M / 2 - 1 - q) * 128, zr[q + M / 2]);
-      ST::st1(dm + (M / 2 - 1 - q) * 128 + n / 2, zi[q]);
+      gio<T>::st1(dm + (M / 2 - 1 - q) * 128, zr[q + M / 2]);
+      gio<T>::st1(dm + (M / 2 - 1 - q) * 128 + n / 2, zi[q]);
     }
   });
 }
 
 // Forward last-pass DC set (slots j 128, j 128 + n/2) from H, stored straight to the global row.
-template <int M, typename T, typename ST = gio<T>>
+template <int M, typename T>
 __device__ __forceinline__ void p3_dc_fwd_direct(const float2* hd, T* d0, int n) {
   constexpr int WS = 4 * 34;
   float d[M];
@@ -253,8 +249,8 @@ __device__ __forceinline__ void p3_dc_fwd_direct(const float2* hd, T* d0, int n)
   rfft_fwd_reg<M>(d);
   ct::static_for<0, M / 2>([&](auto J) {
     constexpr int j = decltype(J)::value;
-    ST::st1(d0 + j * 128, d[j]);
-    ST::st1(d0 + j * 128 + n / 2, d[j + M / 2]);
+    gio<T>::st1(d0 + j * 128, d[j]);
+    gio<T>::st1(d0 + j * 128 + n / 2, d[j + M / 2]);
   });
 }
 
@@ -344,7 +340,6 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
   extern __shared__ float4 smem4[];
   unsigned char* base = reinterpret_cast<unsigned char*>(smem4);
   float2* H = reinterpret_cast<float2*>(base + L::H_OFF);
-  T* O = reinterpret_cast<T*>(base + L::O_OFF);
   float2* TWm = reinterpret_cast<float2*>(base + L::TWM_OFF);
   float2* TWl = reinterpret_cast<float2*>(base + L::TWL_OFF);
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + L::BAR_OFF);
@@ -485,23 +480,11 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
           *reinterpret_cast<float4*>(h1 + i) = make_float4(b[i].x, b[i].y, b[i + 1].x, b[i + 1].y);
         });
       }
-      if (P::O && tid == 0) bulk_wait_read<0>();  // the previous tile's bulk store has read O
       __syncthreads();
       if (NS > 0 && tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
       middle(nv);
       __syncthreads();
-      if constexpr (P::O) {
-        ct::static_for<0, LITEMS>([&](auto RR) {
-          constexpr int r = decltype(RR)::value;
-          constexpr int dv = r * LSTEP;
-          constexpr int off = dv * P::ROWA + 2 * dv;
-          T* ov = O + (vl0 + dv) * P::OROW;
-          if (vl0 + dv < nv)
-            p3_last_set_fwd_direct<P::M3, T, sst1<T>>(lha + off, lhz + off, ltw, ov + qa, ov + qm, kl == P::KL, N);
-        });
-        if (dcl >= 0 && dcl < nv) p3_dc_fwd_direct<P::M3, T, sst1<T>>(lhd, O + dcl * P::OROW, N);
-        fence_proxy_async_smem();
-      } else if constexpr (P::FD) {
+      if constexpr (P::FD) {
         ct::static_for<0, LITEMS>([&](auto RR) {
           constexpr int r = decltype(RR)::value;
           constexpr int dv = r * LSTEP;
@@ -526,7 +509,6 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
       }
     } else {
       last_inv_st(st, nv);  // reads the staged tile directly (no staged -> H copy)
-      if (P::O && tid == 0) bulk_wait_read<0>();  // the previous tile's bulk store has read O
       __syncthreads();
       if (NS > 0 && tid == 0 && nxt < ntiles) stage_issue(x + nxt * VT * (int64_t)N, tile_bytes(nxt), base + sb * P::STAGE, bar + sb);
       middle(nv);
@@ -540,31 +522,15 @@ __global__ void __launch_bounds__(P::NT) rdfft3_kernel(typename P::elem* __restr
           b[i + 1] = make_float2(f.z, f.w);
         });
         rfft_inv_reg<R>(b);
-        if constexpr (P::O) {
-          T* dst = O + v1 * P::OROW + 2 * c1;
-          ct::static_for<0, R>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            sst1<T>::st2(dst + S * i, b[rev_bits<P::LR>(i)]);
-          });
-        } else {
-          T* dst = xt + s1;
-          ct::static_for<0, R>([&](auto I) {
-            constexpr int i = decltype(I)::value;
-            gio<T>::st2(dst + S * i, b[rev_bits<P::LR>(i)]);
-          });
-        }
+        T* dst = xt + s1;
+        ct::static_for<0, R>([&](auto I) {
+          constexpr int i = decltype(I)::value;
+          gio<T>::st2(dst + S * i, b[rev_bits<P::LR>(i)]);
+        });
       }
-      if constexpr (P::O) fence_proxy_async_smem();
     }
     __syncthreads();
-    if constexpr (P::O) {  // O complete: store its rows
-      if (tid == 0) {
-        for (int v = 0; v < nv; ++v) bulk_s2g(xt + (int64_t)v * N, O + v * P::OROW, (uint32_t)(N * sizeof(T)));
-        bulk_commit();
-      }
-    }
   }
-  if (P::O && tid == 0) bulk_wait<0>();
 }
 
 template <typename P, bool kInv>
@@ -580,8 +546,8 @@ bool launch_plan3_dir(typename P::elem* x, int64_t batch, int sms, cudaStream_t 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NT, L::BYTES);
     if (per_sm < 1) per_sm = 1;
     if (verbose())
-      std::fprintf(stderr, "[rdfft] plan3 n=%d VT=%d NSTG=%d O=%d inv=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N,
-                   P::VT, P::NSTG, (int)P::O, (int)kInv, (size_t)L::BYTES, P::NT, per_sm);
+      std::fprintf(stderr, "[rdfft] plan3 n=%d VT=%d NSTG=%d inv=%d: %zu B smem, %d threads, %d CTAs/SM\n", P::N,
+                   P::VT, P::NSTG, (int)kInv, (size_t)L::BYTES, P::NT, per_sm);
   }
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);
@@ -644,9 +610,18 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
     // bf16 n = 2048 forward: the last pass writes an output tile stored by TMA (0.592 -> 0.622 of HBM,
     // 3 CTAs/SM; the inverse through an output tile measured 0.627 -> 0.597 and n = 4096 0.533 / 0.54 ->
     // 0.53 / 0.52, r02_j): both keep the direct stores
+    // n = 2048: the two-pass R = 64 plan (plan2s.cuh) for the bf16 forward (with the output tile, 3
+    // vectors per CTA) and the fp32 inverse; plan3 elsewhere (fraction of HBM, 2^20 vectors, r02_o:
+    // bf16 fwd plan3 0.622 -> plan2s 0.706, fp32 inv 0.916 -> 0.970; bf16 inv 0.631 -> 0.583-0.598 and
+    // fp32 fwd 0.919 -> 0.889-0.924 stay on plan3)
     case 2048:
-      return launch_plan3<Plan3<T, 2048, 4, 1, (sizeof(T) == 4), (sizeof(T) == 2)>, Plan3<T, 2048, 4, 1, true>>(
-          x, batch, inverse, sms, st);
+      if constexpr (sizeof(T) == 2) {
+        if (!inverse) return launch_plan2s_dir<Plan2s<T, 2048, 3, true>, false>(x, batch, sms, st);
+        return launch_plan3_dir<Plan3<T, 2048, 4, 1, true>, true>(x, batch, sms, st);
+      } else {
+        if (inverse) return launch_plan2s_dir<Plan2s<T, 2048, 4>, true>(x, batch, sms, st);
+        return launch_plan3_dir<Plan3<T, 2048, 4, 1, true>, false>(x, batch, sms, st);
+      }
     case 4096: return launch_plan3<Plan3<T, 4096, 2, 1, true>, Plan3<T, 4096, 2, 1, true>>(x, batch, inverse, sms, st);
     case 8192: return launch_planl<PlanL<T, 8192>>(x, batch, inverse, sms, st);
     case 16384: return launch_planl<PlanL<T, 16384>>(x, batch, inverse, sms, st);
