@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck):
+"""Small invocations of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
   compute-sanitizer --tool racecheck python tools/sanitize_run.py
 Transforms n = 2 .. 65536 (plan2, plan2o, plan3, planl, cluster pair), packed products, utilities,
 BCA forward / accumulate / backward on the fused (p = 256, 512, 1024, 2048, 4096), resident-spectra
@@ -27,9 +27,16 @@ for dt in ("bf16", "f32"):
                 c = R.rdfft_decode(x)
                 R.rdfft_encode(c, x)
         torch.cuda.synchronize()
-    if only in ("all", "bca"):
+    if only in ("all", "bca", "bca_synccheck"):
         for (qo, qi, p, T) in ((4, 4, 1024, 9), (3, 3, 256, 11), (2, 2, 512, 7), (1, 1, 2048, 9), (2, 2, 2048, 5),
-                               (1, 1, 4096, 5), (2, 2, 4096, 3), (2, 3, 128, 6), (16, 16, 256, 3)):
+                               (1, 1, 4096, 5), (2, 2, 4096, 3), (2, 3, 128, 6), (16, 16, 256, 3), (3, 3, 512, 5),
+                               (3, 3, 1024, 5)):
+            # bca_synccheck: skip the shapes whose backward runs bca_bwd4_kernel (even q at p = 512; fp32
+            # even q at p = 1024).  It allocates tensor memory and has no mbarrier, which trips synccheck's
+            # "Missing init" report on any such kernel (tools/microbench/synccheck_tmem.cu reproduces it
+            # on a 40-line kernel; profiles/r02_sanitizer.txt); memcheck / racecheck / initcheck cover it.
+            if only == "bca_synccheck" and qo == qi and qo % 2 == 0 and (p == 512 or (p == 1024 and dt == "f32")):
+                continue
             x, w, g = synth.bca_inputs(T, qi * p, qo * p, p, seed=p + qi, dtype=dt, device="cuda")
             y = R.bca_fwd(x, w)
             R.bca_fwd(x, w, y, accumulate=True)
