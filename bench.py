@@ -298,13 +298,17 @@ def run_gpu(args):
     from paper_2511_01385_b200 import rdfft as R
 
     world, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)  # before the process group: NCCL binds each rank to its own GPU
+    dev = torch.device("cuda", local)
     if world > 1:
         # NCCL over NVLink on the box; RDFFT_DIST_BACKEND=gloo lets the N > 1 logic run with several
         # ranks on one GPU (a functional check of sharding / barriers / max-over-ranks / dw all-reduce)
-        dist.init_process_group(os.environ.get("RDFFT_DIST_BACKEND", "nccl"))
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        backend = os.environ.get("RDFFT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group(backend, device_id=dev)
+        else:
+            dist.init_process_group(backend)
     if rank == 0:
         build.build()
     if world > 1:
