@@ -437,6 +437,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
   __syncthreads();
   if constexpr (NC == 2) cooperative_groups::this_cluster().sync();  // peer's H mapped and live
+  // bf16 forward, one vector per CTA: pass 1's element pairs of the NEXT vector are loaded into
+  // registers (32 raw bf16x2 words per thread) right after this vector's pass 1, so their HBM latency
+  // hides behind passes 2 and 3 instead of stalling the next pass 1
+  constexpr bool kPF = (NC == 1 && sizeof(T) == 2 && !kInv);
+  uint32_t pf[kPF ? R : 1];
+  if constexpr (kPF) {
+    if (tid < S / 2 && (int64_t)blockIdx.x < batch) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(x + (int64_t)blockIdx.x * NV) + tid;
+      ct::static_for<0, R>([&](auto I) { pf[decltype(I)::value] = __ldcs(src + (S / 2) * decltype(I)::value); });
+    }
+  }
   for (int64_t v = blockIdx.x / NC; v < batch; v += gridDim.x / NC) {
     T* xv = x + v * NV;
     T* xh = xv + r;  // this CTA's half: elements xh[XS * e], e < N
@@ -446,12 +457,21 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         float2 b[R];
         ct::static_for<0, R>([&](auto I) {
           constexpr int i = decltype(I)::value;
-          if constexpr (NC == 1)
+          if constexpr (kPF)
+            b[rev_bits<5>(i)] = make_float2(__uint_as_float(pf[i] * k65536), __uint_as_float(pf[i] & 0xffff0000u));
+          else if constexpr (NC == 1)
             b[rev_bits<5>(i)] = gio<T>::ld2(xv + 2 * c + S * i, k65536);
           else
             b[rev_bits<5>(i)] = make_float2(gio1<T>::ld(xh + XS * (2 * c + S * i), k65536),
                                             gio1<T>::ld(xh + XS * (2 * c + 1 + S * i), k65536));
         });
+        if constexpr (kPF) {
+          const int64_t vn = v + gridDim.x;
+          if (vn < batch) {
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(x + vn * NV) + c;
+            ct::static_for<0, R>([&](auto I) { pf[decltype(I)::value] = __ldcs(src + (S / 2) * decltype(I)::value); });
+          }
+        }
         rfft_fwd_reg<R>(b);
         const int w0 = rev_bits<P::LS>(2 * c), w1 = w0 + S / 2;
         float* h0 = H + P::phys(w0 * 32);  // a window never crosses a pad boundary
