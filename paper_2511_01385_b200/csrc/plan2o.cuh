@@ -89,47 +89,10 @@ __device__ __forceinline__ void p2o_dc_inv(const P2Roles<P>& r, const __nv_bfloa
   }
 }
 
-// kO: pass 1 writes the real outputs (bf16 pairs, RNE) into an output staging tile O instead of
-// HBM; one thread stores O's rows with TMA bulk copies (the forward's rdfft2fo_kernel scheme).  O
-// rows are skewed by P1 x 4 bytes (the pass-1 width of one vector) so the vectors one store
-// instruction covers fall on disjoint banks.
-template <typename P, bool kO>
-struct P2oSmem {
-  static constexpr int OROW = kO ? P::N + (P::P1 * 4 < 16 ? 16 : P::P1 * 4) / 2 : 0;
-  static constexpr size_t O_OFF = (size_t)P::NSTG * P::STAGE;
-  static constexpr size_t H_OFF = O_OFF + (size_t)P::VT * OROW * 2;
-  static constexpr size_t TW_OFF = H_OFF + (size_t)P::HF * 8;
-  static constexpr size_t BAR_OFF = TW_OFF + (size_t)P::TWF * 8;
-  static constexpr size_t BYTES = BAR_OFF + 8 * P::NSTG;
-  static_assert((OROW * 2) % 16 == 0 && H_OFF % 16 == 0, "16-byte aligned rows");
-};
-
-// inverse pass 1 from H windows into the O tile (bf16 pairs; the values p2_pass1_inv stores to HBM)
-template <typename P, int OROW>
-__device__ __forceinline__ void p2o_pass1_inv_o(const P2Roles<P>& r, __nv_bfloat16* O, int nv) {
-  constexpr int R = P::R, S = P::S;
-  if (r.act1 && r.v1 < nv) {
-    float2 b[R];
-    ct::static_for<0, R / 2>([&](auto I) {
-      constexpr int i = 2 * decltype(I)::value;
-      const float4 f = *reinterpret_cast<const float4*>(r.h1 + i);
-      b[i] = make_float2(f.x, f.y);
-      b[i + 1] = make_float2(f.z, f.w);
-    });
-    rfft_inv_reg<R>(b);
-    __nv_bfloat16* dst = O + r.v1 * OROW + (r.s1 - r.v1 * P::N);
-    ct::static_for<0, R>([&](auto I) {
-      constexpr int i = decltype(I)::value;
-      const __nv_bfloat162 h = __floats2bfloat162_rn(b[rev_bits<P::LR>(i)].x, b[rev_bits<P::LR>(i)].y);
-      *reinterpret_cast<__nv_bfloat162*>(dst + S * i) = h;
-    });
-  }
-}
-
-template <typename P, bool kO = false>
+template <typename P>
 __global__ void __launch_bounds__(P::NTT, 4) rdfft2o_inv_kernel(__nv_bfloat16* __restrict__ x, int64_t batch) {
   using T = __nv_bfloat16;
-  using L = P2oSmem<P, kO>;
+  using L = P2Smem<P>;
   constexpr int VT = P::VT, N = P::N, NS = P::NSTG;
   static_assert(NS >= 1, "staged input");
   extern __shared__ float4 smem4[];
@@ -167,32 +130,19 @@ __global__ void __launch_bounds__(P::NTT, 4) rdfft2o_inv_kernel(__nv_bfloat16* _
     mbar_wait(bar + sb, (it / NS) & 1);
     if (!dcw) p2o_last_inv<P>(r, st, nv, k65536);
     else p2o_dc_inv<P>(r, st, nv, k65536);
-    if (kO && tid == 0) bulk_wait_read<0>();  // the previous tile's bulk store has read O
-    __syncthreads();  // H complete; staging buffer consumed (kO: O free)
+    __syncthreads();  // H complete; staging buffer consumed
     if (tid == 0 && nxt < ntiles)
       stage_issue_rows<P>(x + (int64_t)nxt * VT * N, tile_rows(nxt), base + sb * P::STAGE, bar + sb);
-    if constexpr (kO) {
-      T* O = reinterpret_cast<T*>(base + L::O_OFF);
-      p2o_pass1_inv_o<P, L::OROW>(r, O, nv);
-      fence_proxy_async_smem();
-      __syncthreads();  // O complete; H free for the next tile
-      if (tid == 0) {
-        for (int v = 0; v < nv; ++v) bulk_s2g(xt + (int64_t)v * N, O + v * L::OROW, (uint32_t)(N * 2));
-        bulk_commit();
-      }
-    } else {
-      p2_pass1_inv<P>(r, xt, nv);
-      __syncthreads();  // H free for the next tile
-    }
+    p2_pass1_inv<P>(r, xt, nv);
+    __syncthreads();  // H free for the next tile
   }
-  if (kO && tid == 0) bulk_wait<0>();
 }
 
-template <typename P, bool kO = false>
+template <typename P>
 bool launch_plan2o_inv(__nv_bfloat16* x, int64_t batch, int sms, cudaStream_t st) {
-  using L = P2oSmem<P, kO>;
+  using L = P2Smem<P>;
   if ((reinterpret_cast<uintptr_t>(x) & 15) != 0) return false;
-  auto k = rdfft2o_inv_kernel<P, kO>;
+  auto k = rdfft2o_inv_kernel<P>;
   static int per_sm_dev[kMaxDevices] = {};
   int& per_sm = per_sm_dev[device_index()];
   if (!per_sm) {
@@ -201,8 +151,8 @@ bool launch_plan2o_inv(__nv_bfloat16* x, int64_t batch, int sms, cudaStream_t st
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, P::NTT, L::BYTES);
     if (per_sm < 1) per_sm = 1;
     if (verbose())
-      std::fprintf(stderr, "[rdfft] plan2o inverse n=%d R=%d VT=%d NSTG=%d O=%d: %zu B smem, %d threads, %d CTAs/SM\n",
-                   P::N, P::R, P::VT, P::NSTG, (int)kO, (size_t)L::BYTES, P::NTT, per_sm);
+      std::fprintf(stderr, "[rdfft] plan2o inverse n=%d R=%d VT=%d NSTG=%d: %zu B smem, %d threads, %d CTAs/SM\n",
+                   P::N, P::R, P::VT, P::NSTG, (size_t)L::BYTES, P::NTT, per_sm);
   }
   const int64_t tiles = (batch + P::VT - 1) / P::VT;
   const int grid = (int)(tiles < (int64_t)per_sm * sms ? tiles : (int64_t)per_sm * sms);

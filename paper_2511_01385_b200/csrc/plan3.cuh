@@ -564,22 +564,21 @@ bool launch_plan3(typename PF::elem* x, int64_t batch, bool inverse, int sms, cu
 #define RDFFT_FWD_NSTG 1  // forward staging depth for n = 512 / 1024 (0 = pass 1 straight from HBM)
 #endif
 // Returns true when a specialised kernel was launched for (n, T).
-// bf16 forward, n = 128..1024: the output-staged kernel (rdfft2fo_kernel, plan2.cuh), measured against
+// bf16 forward, n = 256..1024: the output-staged kernel (rdfft2fo_kernel, plan2.cuh), measured against
 // the H -> HBM store phase of rdfft2_kernel (2^20 vectors, fraction of HBM; gpurun_out r02_h):
 // n = 1024 0.721 -> 0.799 (6 vectors per CTA, 4 CTAs/SM; 8 vectors at 3 CTAs/SM: 0.783), 512
-// 0.683 -> 0.710, 256 0.664 -> 0.702, 128 0.615 -> 0.633 (12 vectors per CTA); pass 1 straight from
-// HBM instead of the staging buffer measured 0.58-0.62 at every n.
-// bf16 inverse, n = 128..1024: the staged-read kernel (plan2o.cuh; measured 64 -> 70-76 % of HBM at
-// 512/1024); n = 128 with its pass-1 outputs through an output tile too (0.51 -> 0.60; at 256 .. 1024
-// the output tile measured equal or slower: 0.688 -> 0.684, 0.733 -> 0.717, 0.772 -> 0.703, r02_i).
+// 0.683 -> 0.710, 256 0.664 -> 0.702 (12 vectors per CTA); pass 1 straight from HBM instead of the
+// staging buffer measured 0.58-0.62 at every n.
+// bf16 inverse, n = 256..1024: the staged-read kernel (plan2o.cuh; measured 64 -> 70-76 % of HBM at
+// 512/1024; an output tile for its pass 1 measured equal or slower: 0.688 -> 0.684, 0.733 -> 0.717,
+// 0.772 -> 0.703, r02_i).  (bf16 n = 128 runs the transposing one-vector-per-thread kernel, small.cuh.)
 template <typename T, int N, int R, int VT>
 bool launch_p2(T* x, int64_t batch, bool inverse, int sms, cudaStream_t st) {
-  if constexpr (sizeof(T) == 2 && N >= 128) {
+  if constexpr (sizeof(T) == 2 && N >= 256) {
     if (!inverse) {
       constexpr int VTF = R == 32 ? (N == 1024 ? 6 : VT) : 12;
       return launch_plan2fo<Plan2<T, N, R, VTF, 1>>(x, batch, sms, st);
     }
-    if constexpr (N == 128) return launch_plan2o_inv<Plan2o<N, R, VT, 1>, true>(x, batch, sms, st);
     // n = 256 / 512: 2-deep TMA ring (0.71 -> 0.74 of HBM at 512; at 1024 it costs a CTA per SM:
     // 0.77 -> 0.75; n = 256 0.60 -> 0.68 with the per-width staging skew)
     return launch_plan2o_inv<Plan2o<N, R, VT, ((N == 512 || N == 256) ? 2 : 1)>>(x, batch, sms, st);
@@ -598,12 +597,13 @@ bool launch_rdfft_fast(T* x, int64_t batch, int n, int logn, bool inverse, int s
     case 8: return launch_small<T, 8>(x, batch, inverse, sms, st);
     case 16: return launch_small<T, 16>(x, batch, inverse, sms, st);
     case 32: return launch_small<T, 32>(x, batch, inverse, sms, st);
-    case 64:  // bf16 rows are 128 B (in-register path wins); fp32 rows (256 B) thrash L1 there
-      if (sizeof(T) == 2) return launch_small<T, 64>(x, batch, inverse, sms, st);
-      return launch_plan2<Plan2<T, 64, 16, 32>, Plan2<T, 64, 16, 32>>(x, batch, inverse, sms, st);
-    // fp32 n = 128 / 256: 32 vectors per CTA (measured 0.85 -> 0.96 / 0.87 -> 0.99 of HBM forward);
-    // bf16 keeps 16 (32 measured 0.62 -> 0.56 / 0.66 -> 0.52)
-    case 128: return launch_p2<T, 128, 16, (sizeof(T) == 4 ? 32 : 16)>(x, batch, inverse, sms, st);
+    // n = 64 (both dtypes) and bf16 n = 128: one vector per thread through the per-warp shared-memory
+    // transpose (small.cuh).  Against the two-pass plan (2^20 vectors, fraction of HBM, gpurun_out
+    // r02_y): fp32 n = 64 0.80 / 0.60 -> 0.95 / 0.95, bf16 n = 128 0.64 / 0.60 -> 0.82 / 0.86
+    case 64: return launch_small<T, 64>(x, batch, inverse, sms, st);
+    case 128:
+      if constexpr (sizeof(T) == 2) return launch_small<T, 128>(x, batch, inverse, sms, st);
+      else return launch_p2<T, 128, 16, 32>(x, batch, inverse, sms, st);
     case 256: return launch_p2<T, 256, 16, (sizeof(T) == 4 ? 32 : 16)>(x, batch, inverse, sms, st);
     case 512: return launch_p2<T, 512, 32, 8>(x, batch, inverse, sms, st);
     case 1024: return launch_p2<T, 1024, 32, 8>(x, batch, inverse, sms, st);
