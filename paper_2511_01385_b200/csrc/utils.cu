@@ -148,36 +148,119 @@ __device__ __forceinline__ void ld_pair(const T* p, T& v0, T& v1) {
   }
 }
 
-// packed rows [batch][n] -> interleaved bins [batch][n + 2]: one thread per bin k = 0 .. n/2
+// decode / encode stage the packed rows of a CTA's row chunk in shared memory: the packed side moves
+// with coalesced 16-byte accesses, and the mirrored slot n - k of a bin is read / written in shared
+// memory instead of HBM; the interleaved side moves one bin pair (4 / 8 bytes) per thread, consecutive
+// bins on consecutive lanes.  (One bin per thread straight from HBM with 2-byte mirrored accesses ran
+// at 0.28-0.52 of HBM.)  Rows of at least 16 bytes (n * sizeof(T) % 16 == 0), rows_per_cta * n <= kUSm.
+constexpr int kU = 4;
+constexpr int kUSm = 4096;  // elements of the staged chunk (8 / 16 KB)
+// e / nb for 0 <= e < 2^22 without an integer division: a float-reciprocal estimate and one
+// correction step (the estimate is within one of the true quotient at these magnitudes)
+__device__ __forceinline__ int div_nb(int e, int nb, float inv_nb) {
+  int q = __float2int_rz((float)e * inv_nb);
+  const int r = e - q * nb;
+  q += (r >= nb) - (r < 0);
+  return q;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(kUThreads) decode_kernel(const T* __restrict__ p, T* __restrict__ c, int64_t batch,
-                                                          int n, int rows_per_cta) {
+__global__ void __launch_bounds__(kUThreads) decode_staged_kernel(const T* __restrict__ p, T* __restrict__ c,
+                                                                 int64_t batch, int n, int rows_per_cta) {
+  __shared__ uint4 sm4[kUSm * sizeof(T) / 16];
+  const T* sm = reinterpret_cast<const T*>(sm4);
   const int nb = n / 2 + 1;
   const T zero = T(0.0f);
+  const float inv_nb = 1.0f / (float)nb;
+  constexpr int E = 16 / (int)sizeof(T);
   for (int64_t r0 = (int64_t)blockIdx.x * rows_per_cta; r0 < batch; r0 += (int64_t)gridDim.x * rows_per_cta) {
     const int rows = (int)(batch - r0 < rows_per_cta ? batch - r0 : rows_per_cta);
-    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
-      const int rr = e / nb, k = e - rr * nb;
-      const T* pr = p + (r0 + rr) * (int64_t)n;
-      const T re = pr[k];
-      const T im = (k == 0 || k == n / 2) ? zero : pr[n - k];
-      st_pair<T>(c + (r0 + rr) * (int64_t)(n + 2) + 2 * k, re, im);
+    const uint4* src = reinterpret_cast<const uint4*>(p + r0 * n);
+    __syncthreads();  // the previous chunk's reads of sm are done
+    for (int i = threadIdx.x; i < rows * n / E; i += kUThreads) sm4[i] = __ldcs(src + i);
+    for (int i = rows * n / E * E + threadIdx.x; i < rows * n; i += kUThreads)  // n < E: ragged chunk
+      const_cast<T*>(sm)[i] = p[r0 * n + i];
+    __syncthreads();
+    const int tot = rows * nb;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += kU * kUThreads) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kUThreads;
+        if (e < tot) {
+          const int rr = div_nb(e, nb, inv_nb), k = e - rr * nb;
+          const T* pr = sm + rr * n;
+          const T im = (k == 0 || k == n / 2) ? zero : pr[n - k];
+          st_pair<T>(c + (r0 + rr) * (int64_t)(n + 2) + 2 * k, pr[k], im);
+        }
+      }
     }
   }
 }
 
-// interleaved bins [batch][n + 2] -> packed rows [batch][n]
+// interleaved bins [batch][n + 2] -> packed rows [batch][n] (the mirror of decode_kernel)
 template <typename T>
-__global__ void __launch_bounds__(kUThreads) encode_kernel(const T* __restrict__ c, T* __restrict__ p, int64_t batch,
-                                                          int n, int rows_per_cta) {
+__global__ void __launch_bounds__(kUThreads) encode_staged_kernel(const T* __restrict__ c, T* __restrict__ p,
+                                                                 int64_t batch, int n, int rows_per_cta) {
+  __shared__ uint4 sm4[kUSm * sizeof(T) / 16];
+  T* sm = reinterpret_cast<T*>(sm4);
   const int nb = n / 2 + 1;
+  const float inv_nb = 1.0f / (float)nb;
+  constexpr int E = 16 / (int)sizeof(T);
   for (int64_t r0 = (int64_t)blockIdx.x * rows_per_cta; r0 < batch; r0 += (int64_t)gridDim.x * rows_per_cta) {
     const int rows = (int)(batch - r0 < rows_per_cta ? batch - r0 : rows_per_cta);
-    for (int e = threadIdx.x; e < rows * nb; e += blockDim.x) {
-      const int rr = e / nb, k = e - rr * nb;
+    const int tot = rows * nb;
+    __syncthreads();  // the previous chunk's stores from sm are done
+    for (int e0 = threadIdx.x; e0 < tot; e0 += kU * kUThreads) {
+      T re[kU], im[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kUThreads;
+        if (e < tot) {
+          const int rr = div_nb(e, nb, inv_nb), k = e - rr * nb;
+          ld_pair<T>(c + (r0 + rr) * (int64_t)(n + 2) + 2 * k, re[u], im[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kUThreads;
+        if (e < tot) {
+          const int rr = div_nb(e, nb, inv_nb), k = e - rr * nb;
+          T* pr = sm + rr * n;
+          pr[k] = re[u];
+          if (k != 0 && k != n / 2) pr[n - k] = im[u];
+        }
+      }
+    }
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(p + r0 * n);
+    for (int i = threadIdx.x; i < rows * n / E; i += kUThreads) __stcs(dst + i, sm4[i]);
+    for (int i = rows * n / E * E + threadIdx.x; i < rows * n; i += kUThreads) p[r0 * n + i] = sm[i];  // n < E
+  }
+}
+
+// n > kUSm (one row does not fit the staged chunk): one bin per thread straight from HBM
+template <typename T>
+__global__ void __launch_bounds__(kUThreads) decode_direct_kernel(const T* __restrict__ p, T* __restrict__ c,
+                                                                 int64_t batch, int n) {
+  const int nb = n / 2 + 1;
+  const T zero = T(0.0f);
+  for (int64_t r = blockIdx.x; r < batch; r += gridDim.x) {
+    const T* pr = p + r * n;
+    for (int k = threadIdx.x; k < nb; k += kUThreads) {
+      const T im = (k == 0 || k == n / 2) ? zero : pr[n - k];
+      st_pair<T>(c + r * (int64_t)(n + 2) + 2 * k, pr[k], im);
+    }
+  }
+}
+template <typename T>
+__global__ void __launch_bounds__(kUThreads) encode_direct_kernel(const T* __restrict__ c, T* __restrict__ p,
+                                                                 int64_t batch, int n) {
+  const int nb = n / 2 + 1;
+  for (int64_t r = blockIdx.x; r < batch; r += gridDim.x) {
+    T* pr = p + r * n;
+    for (int k = threadIdx.x; k < nb; k += kUThreads) {
       T re, im;
-      ld_pair<T>(c + (r0 + rr) * (int64_t)(n + 2) + 2 * k, re, im);
-      T* pr = p + (r0 + rr) * (int64_t)n;
+      ld_pair<T>(c + r * (int64_t)(n + 2) + 2 * k, re, im);
       pr[k] = re;
       if (k != 0 && k != n / 2) pr[n - k] = im;
     }
@@ -185,24 +268,49 @@ __global__ void __launch_bounds__(kUThreads) encode_kernel(const T* __restrict__
 }
 
 // a <- a (.) [conj] b per bin for rows longer than the tiled kernel's 16 KB tiles (n > 4096):
-// one thread per bin k = 0 .. n/2 of a row, (slot k, slot n - k) pairs.
+// bins k = 0 .. n/2 of a row, (slot k, slot n - k) pairs; kU bins per thread per step with
+// all loads issued before the first store (decode_kernel's schedule).
 template <typename T, bool kConj>
 __global__ void __launch_bounds__(kUThreads) packed_mul_large_kernel(T* __restrict__ a, const T* __restrict__ b,
                                                                     int64_t batch, int n, bool bcast) {
   const int nb = n / 2 + 1;
   const int64_t total = batch * nb;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / nb;
-    const int k = (int)(e - r * nb);
-    T* ar = a + r * n;
-    const T* br = b + (bcast ? 0 : r * n);
-    if (k == 0 || k == n / 2) {  // real bins
-      ar[k] = (T)((float)ar[k] * (float)br[k]);
-    } else {
-      const float xr = (float)ar[k], xi = (float)ar[n - k];
-      const float yr = (float)br[k], yi = kConj ? -(float)br[n - k] : (float)br[n - k];
-      ar[k] = (T)fmaf(xr, yr, -xi * yi);
-      ar[n - k] = (T)fmaf(xr, yi, xi * yr);
+  const int64_t step = (int64_t)gridDim.x * kUThreads;
+  const double inv_nb = 1.0 / (double)nb;
+  for (int64_t e0 = blockIdx.x * (int64_t)kUThreads + threadIdx.x; e0 < total; e0 += kU * step) {
+    float xr[kU], xi[kU], yr[kU], yi[kU];
+    T* ar[kU];
+    int kk[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t e = e0 + u * step;
+      ar[u] = nullptr;
+      if (e < total) {
+        int64_t r = (int64_t)((double)e * inv_nb);  // e / nb: fp64 reciprocal + one correction (e < 2^50)
+        int k = (int)(e - r * nb);
+        if (k >= nb) { ++r; k -= nb; }
+        if (k < 0) { --r; k += nb; }
+        ar[u] = a + r * n;
+        kk[u] = k;
+        const T* br = b + (bcast ? 0 : r * n);
+        const bool real = (k == 0 || k == n / 2);
+        xr[u] = (float)ar[u][k];
+        yr[u] = (float)br[k];
+        xi[u] = real ? 0.f : (float)ar[u][n - k];
+        yi[u] = real ? 0.f : (kConj ? -(float)br[n - k] : (float)br[n - k]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (ar[u] != nullptr) {
+        const int k = kk[u];
+        if (k == 0 || k == n / 2) {  // real bins
+          ar[u][k] = (T)(xr[u] * yr[u]);
+        } else {
+          ar[u][k] = (T)fmaf(xr[u], yr[u], -xi[u] * yi[u]);
+          ar[u][n - k] = (T)fmaf(xr[u], yi[u], xi[u] * yr[u]);
+        }
+      }
     }
   }
 }
@@ -230,17 +338,27 @@ void launch_packed_axpy(T* y, const T* x, float alpha, int64_t batch, int n, boo
 }
 template <typename T>
 void launch_decode(const T* p, T* c, int64_t batch, int n, int sms, cudaStream_t st) {
-  const int rows = n >= 1024 ? 1 : 1024 / n;
+  if (n > kUSm) {
+    const int grid = (int)(batch < (int64_t)sms * 8 ? batch : (int64_t)sms * 8);
+    decode_direct_kernel<T><<<grid, kUThreads, 0, st>>>(p, c, batch, n);
+    return;
+  }
+  const int rows = kUSm / n;
   const int64_t ctas = (batch + rows - 1) / rows;
   const int grid = (int)(ctas < (int64_t)sms * 8 ? ctas : (int64_t)sms * 8);
-  decode_kernel<T><<<grid, kUThreads, 0, st>>>(p, c, batch, n, rows);
+  decode_staged_kernel<T><<<grid, kUThreads, 0, st>>>(p, c, batch, n, rows);
 }
 template <typename T>
 void launch_encode(const T* c, T* p, int64_t batch, int n, int sms, cudaStream_t st) {
-  const int rows = n >= 1024 ? 1 : 1024 / n;
+  if (n > kUSm) {
+    const int grid = (int)(batch < (int64_t)sms * 8 ? batch : (int64_t)sms * 8);
+    encode_direct_kernel<T><<<grid, kUThreads, 0, st>>>(c, p, batch, n);
+    return;
+  }
+  const int rows = kUSm / n;
   const int64_t ctas = (batch + rows - 1) / rows;
   const int grid = (int)(ctas < (int64_t)sms * 8 ? ctas : (int64_t)sms * 8);
-  encode_kernel<T><<<grid, kUThreads, 0, st>>>(c, p, batch, n, rows);
+  encode_staged_kernel<T><<<grid, kUThreads, 0, st>>>(c, p, batch, n, rows);
 }
 
 template <typename T>

@@ -315,14 +315,32 @@ def test_large_n_packed_mul(dtype, conj):
 
 # ------------------------------------------------ packed-spectrum utilities
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-@pytest.mark.parametrize("n", [2, 4, 8, 16, 64, 1024, 4096])
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64, 1024, 4096, 16384])
 def test_decode_encode_bit_exact(n, dtype):
-    """decode / encode are permutations (plus the two explicit zeros): bit-exact vs the oracle."""
+    """decode / encode are permutations (plus the two explicit zeros): bit-exact vs the oracle
+    (n <= 4096: rows staged through shared memory in chunks of 4096 elements, a ragged last chunk;
+    n = 16384: the per-bin kernel)."""
     b = max(3, (1 << 14) // n) + 3
     p = synth.randn((b, n), seed=200 + n, dtype=dtype).cuda()
     c = R.rdfft_decode(p)
     torch.cuda.synchronize()
     assert np.array_equal(f64(c), o.decode(f64(p)))
+    p2 = R.rdfft_encode(c)
+    torch.cuda.synchronize()
+    assert torch.equal(p2, p)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("n", [4, 256])
+def test_decode_encode_many_chunks_per_cta(n, dtype):
+    """Enough rows that every CTA walks several staged chunks (the persistent loop reuses the shared
+    tile): bit-exact against the oracle on sampled rows, encode(decode(p)) == p on all of them."""
+    b = (1 << 22) // n + 7
+    p = synth.randn((b, n), seed=210 + n, dtype=dtype).cuda()
+    c = R.rdfft_decode(p)
+    torch.cuda.synchronize()
+    idx = np.unique(np.r_[0, 1, b - 1, b - 2, np.random.default_rng(n).integers(0, b, 256)])
+    assert np.array_equal(f64(c)[idx], o.decode(f64(p)[idx]))
     p2 = R.rdfft_encode(c)
     torch.cuda.synchronize()
     assert torch.equal(p2, p)
