@@ -44,12 +44,24 @@ __global__ void __launch_bounds__(kUThreads) packed_conj_kernel(T* __restrict__ 
     const int64_t e0 = v * E;  // a vector may span several rows when n < E
     uint4 u = __ldcs(a4 + v);
     uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    if (n >= 2 * E) {
+      // the 16-byte vector holds E consecutive columns c0 .. c0 + E - 1 of one row, and n/2 is a multiple
+      // of E: every column flips (c0 > n/2), none does (c0 < n/2), or all but the first (c0 == n/2)
+      const int c0 = (int)(e0 & (n - 1));
+      const uint32_t m = c0 >= n / 2 ? (sizeof(T) == 4 ? 0x80000000u : 0x80008000u) : 0u;
+      w[0] ^= (c0 == n / 2) ? (sizeof(T) == 4 ? 0u : 0x80000000u) : m;
+      w[1] ^= m;
+      w[2] ^= m;
+      w[3] ^= m;
+    } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if constexpr (sizeof(T) == 4) {
-        w[i] ^= neg_bit<T>((int)((e0 + i) & (n - 1)), n);
-      } else {
-        w[i] ^= neg_bit<T>((int)((e0 + 2 * i) & (n - 1)), n) | (neg_bit<T>((int)((e0 + 2 * i + 1) & (n - 1)), n) << 16);
+      for (int i = 0; i < 4; ++i) {
+        if constexpr (sizeof(T) == 4) {
+          w[i] ^= neg_bit<T>((int)((e0 + i) & (n - 1)), n);
+        } else {
+          w[i] ^= neg_bit<T>((int)((e0 + 2 * i) & (n - 1)), n) |
+                  (neg_bit<T>((int)((e0 + 2 * i + 1) & (n - 1)), n) << 16);
+        }
       }
     }
     __stcs(a4 + v, make_uint4(w[0], w[1], w[2], w[3]));
