@@ -26,10 +26,12 @@ def main():
     ap.add_argument("--shapes", default="roberta_base,roberta_large,llama2_7b")
     ap.add_argument("--dtypes", default="bf16,f32")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--tokens", default="", help="comma list of T overriding the shapes' T (fixed-cost / wave scaling)")
     a = ap.parse_args()
     build.build()
     for name in a.shapes.split(","):
-        T, d, p = SHAPES[name]
+      T0, d, p = SHAPES[name]
+      for T in ([int(t) for t in a.tokens.split(",")] if a.tokens else [T0]):
         for dt in a.dtypes.split(","):
             s = 2 if dt == "bf16" else 4
             nbuf = max(2, int(2 * 126e6 // (3 * T * d * s)) + 1)  # rotate buffer sets so L2 cannot hold them
