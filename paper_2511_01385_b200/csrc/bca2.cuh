@@ -175,32 +175,27 @@ __global__ void __launch_bounds__(P::NT, 1) bca_fwd2_kernel(const typename P::el
   const P2Roles<P> rh(H, TWf, TWi, tid);
   auto tile_rows = [&](int64_t t) { return (int)((T_ - t * TT < TT ? T_ - t * TT : TT) * q); };
   __syncthreads();
-  // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors, into the resident region (or the caller's
-  // resident spectra copied in: wspec)
-  if (wspec) {
-    p2_load_spectra<P>(Wr, wspec, q * q, tid, P::NT);
-  } else {
-    if constexpr (L::STAGES > 0) {
-      if (tid == 0) stage_issue_rows<P>(w, q * q, base, bar);
-      mbar_wait(bar, 0);
-    }
-    const P2Roles<P> rw(Wr, TWf, TWi, tid);
-    if constexpr (L::STAGES > 0)
-      p2_pass1_fwd<P>(rw, reinterpret_cast<const T*>(base), q * q, k65536);
-    else
-      p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
-    __syncthreads();
-    p2_last_fwd<P>(rw, q * q);
-    p2_dc_fwd<P>(rw, q * q);
-  }
-  __syncthreads();
-  uint32_t phase_use[2] = {wspec ? 0u : 1u, 0};  // stage 0 has completed one phase (the weights)
+  // the first tiles' TMA loads go out before the weight prologue, so their latency overlaps it (issued
+  // after the prologue they added a load latency to every launch; RoBERTa-base forward ~1.5 us)
   if (tid == 0) {
     for (int s = 0; s < L::STAGES; ++s) {
       const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
       if (t < ntiles) stage_issue_rows<P>(x + t * TT * tok_elems, tile_rows(t), base + s * P::STAGE, bar + s);
     }
   }
+  // ---- prologue: W_ij = rdFFT(w_ij), q*q <= VT vectors (read straight from HBM), into the resident
+  // region (or the caller's resident spectra copied in: wspec)
+  if (wspec) {
+    p2_load_spectra<P>(Wr, wspec, q * q, tid, P::NT);
+  } else {
+    const P2Roles<P> rw(Wr, TWf, TWi, tid);
+    p2_pass1_fwd<P, true>(rw, w, q * q, k65536);
+    __syncthreads();
+    p2_last_fwd<P>(rw, q * q);
+    p2_dc_fwd<P>(rw, q * q);
+  }
+  __syncthreads();
+  uint32_t phase_use[2] = {0, 0};
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int ntok = (int)(T_ - tile * TT < TT ? T_ - tile * TT : TT);
@@ -626,6 +621,39 @@ __global__ void __launch_bounds__(P::NT, 1) bca_bwd3_kernel(const typename P::el
     __syncthreads();
     p2_pass1_inv<P>(rx, dx + e0, nv);  // g rows of this tile are already consumed
     __syncthreads();
+  }
+  // token split (TS > 1 threads per item, p = 256): the TS partial accumulators of an item are summed
+  // in shared memory (Hx is free after the last tile) so only one thread per item issues the atomics —
+  // the flush's atomics land on q^2 p addresses from every CTA (RoBERTa-base: 444 CTAs), and halving
+  // them took the RoBERTa-base backward from 61.8 to 57.6 us (the whole flush cost ~5 us; r02_dd)
+  if constexpr (!kAccS && TS > 1) {
+    float4* red = reinterpret_cast<float4*>(Hx);  // [ts - 1][i][j][item]
+    static_assert((size_t)(TS - 1) * Q * Q * NI * 16 <= (size_t)P::HF * 8, "reduction buffer fits in Hx");
+    const int ts = tid / NI, item = tid % NI;
+    if (ts > 0) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+          if (i < q && j < q)
+            red[(((ts - 1) * Q + i) * Q + j) * NI + item] =
+                make_float4(acc[0][i][j].b1.x, acc[0][i][j].b1.y, acc[0][i][j].b2.x, acc[0][i][j].b2.y);
+    }
+    __syncthreads();
+    if (ts > 0) return;
+#pragma unroll
+    for (int t2 = 1; t2 < TS; ++t2)
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+#pragma unroll
+        for (int j = 0; j < Q; ++j)
+          if (i < q && j < q) {
+            const float4 f = red[(((t2 - 1) * Q + i) * Q + j) * NI + item];
+            acc[0][i][j].b1.x += f.x;
+            acc[0][i][j].b1.y += f.y;
+            acc[0][i][j].b2.x += f.z;
+            acc[0][i][j].b2.y += f.w;
+          }
   }
 #pragma unroll
   for (int a = 0; a < IPT; ++a) {
