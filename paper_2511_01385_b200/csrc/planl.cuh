@@ -58,7 +58,16 @@ struct PlanL {
   static constexpr int TWCA = N / 256, TWCB = 128;
   static constexpr size_t TWC_OFF = BYTES1;
   static constexpr size_t BYTES2 = TWC_OFF + (size_t)(TWCA + TWCB) * 8;
-  static constexpr size_t BYTES = BYTES1;
+  // kST (one-CTA plan, one pass-3 set per thread: n = 32768): pass 3's natural-order side is a row
+  // staged in shared memory at H's start (it aliases H: a barrier separates pass 3's reads of H from its
+  // writes) — the forward's outputs leave through TMA bulk stores, the inverse's inputs arrive by a TMA
+  // bulk load issued as soon as the previous vector's pass 1 has read H — instead of one 2-byte
+  // global access per slot (lg_throttle-bound at one CTA per SM).  mbarrier at BAR_OFF.
+  static constexpr bool kST = (K3PT == 1);
+  static constexpr size_t BAR_OFF = BYTES1;
+  static constexpr size_t BYTES = BYTES1 + 16;
+  static_assert((size_t)N * sizeof(T) <= (size_t)N * 4, "the staged row fits in H");
+  static_assert(!kST || S / 2 == NT, "kST: every thread runs pass 1 (barriers inside it)");
   static_assert(M3 >= 8 && M3 <= 32 && LS >= 8, "plan L shape");
   static_assert(4 * NT == (N >> 4), "store/load phase chunk i sits in pad period i");
   static_assert(NW2 % (2 * (N / 4096)) == 0, "pass-2 half-warp block pairing");
@@ -105,16 +114,18 @@ struct LTw3 {
 // (= be + j m0 + k) and pb[OFF::b(j)] (= be + (j+1) m0 - k).  half (k == m0/2, the zero-imaginary
 // set): both are the same slot; kHalfB: read it through pb (the pass-3 half set, whose pad follows
 // b()).  tw.template at<r>() = W_W^{k r} (forward) / conj (inverse).
-// kG (pass 3 of the one-CTA plan): the forward stores its outputs straight to the global row and the
-// inverse reads its inputs straight from it — slot be + j m0 + k at ga[j m0], slot be + (j+1) m0 - k
-// at gb[(j+1) m0] (ga = row + k, gb = row - k) — instead of going through H and a chunked phase.
-template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false, typename TW>
-__device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW& tw,
-                                       typename P::elem* ga = nullptr, typename P::elem* gb = nullptr,
-                                       int m0 = 0, uint32_t k65536 = 0) {
-  using T = typename P::elem;
+// kG (pass 3 of the one-CTA plan): the forward stores its outputs to a natural-order row and the
+// inverse reads its inputs from one — slot be + j m0 + k at ga[j m0], slot be + (j+1) m0 - k at
+// gb[(j+1) m0] (ga = row + k, gb = row - k) — instead of H: the global row itself (ST = gio<T>,
+// LD = gio1<T>) or the staged row in shared memory (ST = sst1<T>, LD = sio1<T>; PlanL::kST).
+// Split in two phases so the staged pass 3 can put a barrier between them: pl_set_in reads the set
+// and runs its arithmetic into (zr, zi), pl_set_out writes the results.
+template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false,
+          typename LD = gio1<typename P::elem>, typename TW>
+__device__ __forceinline__ void pl_set_in(float (&zr)[M], float (&zi)[M], float* pa, float* pb, bool half,
+                                          const TW& tw, const typename P::elem* ga = nullptr,
+                                          const typename P::elem* gb = nullptr, int m0 = 0, uint32_t k65536 = 0) {
   constexpr int LM = ilog2c<M>();
-  float zr[M], zi[M];
   auto A = [&](auto J) -> float& {
     constexpr int j = decltype(J)::value;
     if constexpr (kHalfB) return pb[OFF::b(j)];
@@ -139,29 +150,6 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
       zi[j] = fmaf(q, t.y, zi[j] * t.x);
     });
     cfft_dit<M>(zr, zi);
-    // slot be + q m0 + k <- (q < M/2 ? Re : -Im) Y[q];  be + (M - q) m0 - k (= B(M-1-q)) <- the other
-    ct::static_for<0, M>([&](auto Q) {
-      constexpr int q = decltype(Q)::value;
-      if constexpr (kG) {
-        if constexpr (q < M / 2) {
-          gio<T>::st1(ga + q * m0, zr[q]);
-          gio<T>::st1(gb + (M - q) * m0, zi[q]);
-        } else if constexpr (!kHalfB) {
-          if (!half) {
-            gio<T>::st1(ga + q * m0, -zi[q]);
-            gio<T>::st1(gb + (M - q) * m0, zr[q]);
-          }
-        }
-      } else if constexpr (q < M / 2) {  // (half set: B(M-1-q) is another slot of the same set)
-        A(Q) = zr[q];
-        B(ct::ic<M - 1 - q>{}) = zi[q];
-      } else if constexpr (!kHalfB) {
-        if (!half) {
-          A(Q) = -zi[q];
-          B(ct::ic<M - 1 - q>{}) = zr[q];
-        }
-      }
-    });
   } else {
     // Y[q] into register rev(q): q < M/2: Re at A(q), Im at B(M-1-q); q >= M/2: Re at B(M-1-q),
     // Im = -(value at A(q)).  Half set: A(q) = B(q) real for q < M/2 (mirror of the forward).
@@ -169,7 +157,7 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
       constexpr int q = decltype(Q)::value;
       constexpr int rq = rev_bits<LM>(q);
       if constexpr (kG) {
-        const float av = gio1<T>::ld(ga + q * m0, k65536), bv = gio1<T>::ld(gb + (M - q) * m0, k65536);
+        const float av = LD::ld(ga + q * m0, k65536), bv = LD::ld(gb + (M - q) * m0, k65536);
         if constexpr (q < M / 2) {
           zr[rq] = av;
           zi[rq] = bv;
@@ -205,6 +193,49 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
       zr[rj] = fmaf(q, t.x, -zi[rj] * t.y);
       zi[rj] = fmaf(q, t.y, zi[rj] * t.x);
     });
+  }
+}
+
+template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false,
+          typename ST = gio<typename P::elem>>
+__device__ __forceinline__ void pl_set_out(const float (&zr)[M], const float (&zi)[M], float* pa, float* pb,
+                                           bool half, typename P::elem* ga = nullptr, typename P::elem* gb = nullptr,
+                                           int m0 = 0) {
+  constexpr int LM = ilog2c<M>();
+  auto A = [&](auto J) -> float& {
+    constexpr int j = decltype(J)::value;
+    if constexpr (kHalfB) return pb[OFF::b(j)];
+    else return pa[OFF::a(j)];
+  };
+  auto B = [&](auto J) -> float& {
+    constexpr int j = decltype(J)::value;
+    return pb[OFF::b(j)];
+  };
+  if (!kInv) {
+    // slot be + q m0 + k <- (q < M/2 ? Re : -Im) Y[q];  be + (M - q) m0 - k (= B(M-1-q)) <- the other
+    ct::static_for<0, M>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      if constexpr (kG) {
+        if constexpr (q < M / 2) {
+          ST::st1(ga + q * m0, zr[q]);
+          ST::st1(gb + (M - q) * m0, zi[q]);
+        } else if constexpr (!kHalfB) {
+          if (!half) {
+            ST::st1(ga + q * m0, -zi[q]);
+            ST::st1(gb + (M - q) * m0, zr[q]);
+          }
+        }
+      } else if constexpr (q < M / 2) {  // (half set: B(M-1-q) is another slot of the same set)
+        A(Q) = zr[q];
+        B(ct::ic<M - 1 - q>{}) = zi[q];
+      } else if constexpr (!kHalfB) {
+        if (!half) {
+          A(Q) = -zi[q];
+          B(ct::ic<M - 1 - q>{}) = zr[q];
+        }
+      }
+    });
+  } else {
     ct::static_for<0, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
       constexpr int rj = rev_bits<LM>(j);
@@ -216,26 +247,45 @@ __device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW
   }
 }
 
-// DC set of pass 3 with the global row on one side (kG): forward H -> row, inverse row -> H.
-template <typename P, int M, bool kInv, typename OFF>
-__device__ __forceinline__ void pl_dc_g(float* p0, typename P::elem* g0, int m0, float scale, uint32_t k65536) {
-  using T = typename P::elem;
-  float d[M];
+template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false, typename TW>
+__device__ __forceinline__ void pl_set(float* pa, float* pb, bool half, const TW& tw,
+                                       typename P::elem* ga = nullptr, typename P::elem* gb = nullptr,
+                                       int m0 = 0, uint32_t k65536 = 0) {
+  float zr[M], zi[M];
+  pl_set_in<P, M, kInv, OFF, kHalfB, kG>(zr, zi, pa, pb, half, tw, ga, gb, m0, k65536);
+  pl_set_out<P, M, kInv, OFF, kHalfB, kG>(zr, zi, pa, pb, half, ga, gb, m0);
+}
+
+// DC set of pass 3 with a natural-order row on one side (kG): forward H -> row, inverse row -> H;
+// the row is the global one (LD = gio1, ST = gio) or the staged one in shared memory (sio1, sst1).
+template <typename P, int M, bool kInv, typename OFF, typename LD = gio1<typename P::elem>>
+__device__ __forceinline__ void pl_dc_g_in(float (&d)[M], const float* p0, const typename P::elem* g0, int m0,
+                                           uint32_t k65536) {
   ct::static_for<0, M>([&](auto J) {
     constexpr int j = decltype(J)::value;
-    d[j] = kInv ? gio1<T>::ld(g0 + j * m0, k65536) : p0[OFF::a(j)];
+    d[j] = kInv ? LD::ld(g0 + j * m0, k65536) : p0[OFF::a(j)];
   });
   if (!kInv)
     rfft_fwd_reg<M>(d);
   else
     rfft_inv_reg<M>(d);
+}
+template <typename P, int M, bool kInv, typename OFF, typename ST = gio<typename P::elem>>
+__device__ __forceinline__ void pl_dc_g_out(const float (&d)[M], float* p0, typename P::elem* g0, int m0,
+                                            float scale) {
   ct::static_for<0, M>([&](auto J) {
     constexpr int j = decltype(J)::value;
     if (!kInv)
-      gio<T>::st1(g0 + j * m0, d[j] * scale);
+      ST::st1(g0 + j * m0, d[j] * scale);
     else
       p0[OFF::a(j)] = d[j] * scale;
   });
+}
+template <typename P, int M, bool kInv, typename OFF>
+__device__ __forceinline__ void pl_dc_g(float* p0, typename P::elem* g0, int m0, float scale, uint32_t k65536) {
+  float d[M];
+  pl_dc_g_in<P, M, kInv, OFF>(d, p0, g0, m0, k65536);
+  pl_dc_g_out<P, M, kInv, OFF>(d, p0, g0, m0, scale);
 }
 
 // DC set: slots p0[OFF::a(j)] (j < M) — the packed real M-point FFT (inverse: unscaled x scale).
@@ -287,62 +337,113 @@ struct gio4<__nv_bfloat16> {
 
 // Cluster-pair cross stage (m = N, the vector has 2N slots), forward: groups k in this CTA's
 // quarter, A from window 0 (H0), B from window 1 (H1), outputs straight to the global row xv.
+// U groups per batch: all their shared (local and peer) loads first, then the arithmetic and the
+// stores — the generic stores would otherwise keep the compiler from hoisting the next group's loads.
 template <typename P>
 __device__ __forceinline__ void pl_cross_fwd(const float* H0, const float* H1, const float2* TWCa, float2 twb,
                                              typename P::elem* xv, int r, int tid) {
   using T = typename P::elem;
-  constexpr int m = P::N, NT = P::NT, Q = m / 4;
-#pragma unroll 2
-  for (int i = 0; i < Q / NT; ++i) {
-    const int k = r * Q + tid + NT * i;
-    if (k == 0) {  // k = 0: (a, b) -> (a + b, a - b); k = m/2: slot m/2 kept, slot 3m/2 negated
-      const float a = H0[P::phys(0)], b = H1[P::phys(0)];
-      gio<T>::st1(xv, a + b);
-      gio<T>::st1(xv + m, a - b);
-      gio<T>::st1(xv + m / 2, H0[P::phys(m / 2)]);
-      gio<T>::st1(xv + 3 * m / 2, -H1[P::phys(m / 2)]);
-      continue;
-    }
-    const float2 ta = TWCa[k >> 7];  // W_{2m}^k = W^{128 a} W^b, b = k % 128 (fixed per thread)
-    const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
-    const float ar = H0[P::phys(k)], ai = H0[P::phys(m - k)];
-    const float br = H1[P::phys(k)], bi = H1[P::phys(m - k)];
-    const float ur = fmaf(br, wr, -bi * wi), ui = fmaf(br, wi, bi * wr);
-    gio<T>::st1(xv + k, ar + ur);
-    gio<T>::st1(xv + 2 * m - k, ai + ui);
-    gio<T>::st1(xv + m - k, ar - ur);
-    gio<T>::st1(xv + m + k, ui - ai);
+  constexpr int m = P::N, NT = P::NT, Q = m / 4, U = 4;
+  static_assert((Q / NT) % U == 0, "cross-stage batches");
+#pragma unroll 1
+  for (int i0 = 0; i0 < Q / NT; i0 += U) {
+    float ar[U], ai[U], br[U], bi[U];
+    float2 ta[U];
+    ct::static_for<0, U>([&](auto I) {
+      constexpr int u = decltype(I)::value;
+      const int k = r * Q + tid + NT * (i0 + u);
+      const int kk = k == 0 ? m / 2 : k;  // k = 0 is handled below (its mirror slots are not a group)
+      ar[u] = H0[P::phys(kk)];
+      ai[u] = H0[P::phys(m - kk)];
+      br[u] = H1[P::phys(kk)];
+      bi[u] = H1[P::phys(m - kk)];
+      ta[u] = TWCa[kk >> 7];  // W_{2m}^k = W^{128 a} W^b, b = k % 128 (fixed per thread)
+    });
+    ct::static_for<0, U>([&](auto I) {
+      constexpr int u = decltype(I)::value;
+      const int k = r * Q + tid + NT * (i0 + u);
+      if (k == 0) {  // k = 0: (a, b) -> (a + b, a - b); k = m/2: slot m/2 kept, slot 3m/2 negated
+        const float a = H0[P::phys(0)], b = H1[P::phys(0)];
+        gio<T>::st1(xv, a + b);
+        gio<T>::st1(xv + m, a - b);
+        gio<T>::st1(xv + m / 2, H0[P::phys(m / 2)]);
+        gio<T>::st1(xv + 3 * m / 2, -H1[P::phys(m / 2)]);
+      } else {
+        const float wr = ta[u].x * twb.x - ta[u].y * twb.y, wi = ta[u].x * twb.y + ta[u].y * twb.x;
+        const float ur = fmaf(br[u], wr, -bi[u] * wi), ui = fmaf(br[u], wi, bi[u] * wr);
+        gio<T>::st1(xv + k, ar[u] + ur);
+        gio<T>::st1(xv + 2 * m - k, ai[u] + ui);
+        gio<T>::st1(xv + m - k, ar[u] - ur);
+        gio<T>::st1(xv + m + k, ui - ai[u]);
+      }
+    });
   }
 }
 
 // Cluster-pair cross stage, inverse (Eq. 7's first stage, with its 1/2): global row -> H0, H1.
+// Batched like the forward: U groups' HBM loads in flight before any shared store.
 template <typename P>
 __device__ __forceinline__ void pl_cross_inv(float* H0, float* H1, const float2* TWCa, float2 twb,
                                              const typename P::elem* xv, int r, int tid, uint32_t k65536) {
   using T = typename P::elem;
-  constexpr int m = P::N, NT = P::NT, Q = m / 4;
-#pragma unroll 2
-  for (int i = 0; i < Q / NT; ++i) {
-    const int k = r * Q + tid + NT * i;
-    if (k == 0) {
-      const float s = gio1<T>::ld(xv, k65536), d = gio1<T>::ld(xv + m, k65536);
-      H0[P::phys(0)] = 0.5f * (s + d);
-      H1[P::phys(0)] = 0.5f * (s - d);
-      H0[P::phys(m / 2)] = gio1<T>::ld(xv + m / 2, k65536);
-      H1[P::phys(m / 2)] = -gio1<T>::ld(xv + 3 * m / 2, k65536);
-      continue;
-    }
-    const float2 ta = TWCa[k >> 7];  // conj(W_{2m}^k)
-    const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
-    const float ykr = gio1<T>::ld(xv + k, k65536), yki = gio1<T>::ld(xv + 2 * m - k, k65536);
-    const float ymr = gio1<T>::ld(xv + m - k, k65536), ymi = -gio1<T>::ld(xv + m + k, k65536);
-    const float dr = 0.5f * (ykr - ymr), di = 0.5f * (yki - ymi);
-    H0[P::phys(k)] = 0.5f * (ykr + ymr);
-    H0[P::phys(m - k)] = 0.5f * (yki + ymi);
-    H1[P::phys(k)] = fmaf(dr, wr, -di * wi);
-    H1[P::phys(m - k)] = fmaf(dr, wi, di * wr);
+  constexpr int m = P::N, NT = P::NT, Q = m / 4, U = 8;
+  static_assert((Q / NT) % U == 0, "cross-stage batches");
+#pragma unroll 1
+  for (int i0 = 0; i0 < Q / NT; i0 += U) {
+    float ykr[U], yki[U], ymr[U], ymi[U];
+    ct::static_for<0, U>([&](auto I) {
+      constexpr int u = decltype(I)::value;
+      const int k = r * Q + tid + NT * (i0 + u);
+      const int kk = k == 0 ? m / 2 : k;  // k = 0 is handled below (slot 2m - 0 is outside the row)
+      ykr[u] = gio1<T>::ld(xv + kk, k65536);
+      yki[u] = gio1<T>::ld(xv + 2 * m - kk, k65536);
+      ymr[u] = gio1<T>::ld(xv + m - kk, k65536);
+      ymi[u] = -gio1<T>::ld(xv + m + kk, k65536);
+    });
+    ct::static_for<0, U>([&](auto I) {
+      constexpr int u = decltype(I)::value;
+      const int k = r * Q + tid + NT * (i0 + u);
+      if (k == 0) {
+        const float s = gio1<T>::ld(xv, k65536), d = gio1<T>::ld(xv + m, k65536);
+        H0[P::phys(0)] = 0.5f * (s + d);
+        H1[P::phys(0)] = 0.5f * (s - d);
+        H0[P::phys(m / 2)] = ykr[u];   // slot m/2
+        H1[P::phys(m / 2)] = -yki[u];  // -(slot 3m/2)
+      } else {
+        const float2 ta = TWCa[k >> 7];  // conj(W_{2m}^k)
+        const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
+        const float dr = 0.5f * (ykr[u] - ymr[u]), di = 0.5f * (yki[u] - ymi[u]);
+        H0[P::phys(k)] = 0.5f * (ykr[u] + ymr[u]);
+        H0[P::phys(m - k)] = 0.5f * (yki[u] + ymi[u]);
+        H1[P::phys(k)] = fmaf(dr, wr, -di * wi);
+        H1[P::phys(m - k)] = fmaf(dr, wi, di * wr);
+      }
+    });
   }
 }
+
+// Cluster pair, pass 1: elements 4 g + r and 4 g + 2 + r of the row (the two subsequences 2c, 2c + 1 of
+// this CTA's half x[r :: 2]) from one 8-byte (bf16) / 16-byte (fp32) load of the 4-element group at p —
+// half the load instructions of two strided scalar loads; the peer CTA uses the other two elements.
+template <typename T>
+struct pair_ld;
+template <>
+struct pair_ld<__nv_bfloat16> {
+  __device__ __forceinline__ static float2 ld(const __nv_bfloat16* p, uint32_t sel) {
+    const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));
+    return make_float2(__uint_as_float(__byte_perm(u.x, 0u, sel)), __uint_as_float(__byte_perm(u.y, 0u, sel)));
+  }
+  // selector: result bytes (0, 0, e_r lo, e_r hi), e_r = bytes 2r, 2r + 1 of the word
+  __device__ __forceinline__ static uint32_t sel(int r) { return r ? 0x3244u : 0x1044u; }
+};
+template <>
+struct pair_ld<float> {
+  __device__ __forceinline__ static float2 ld(const float* p, uint32_t sel) {
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+    return sel ? make_float2(v.y, v.w) : make_float2(v.x, v.z);
+  }
+  __device__ __forceinline__ static uint32_t sel(int r) { return (uint32_t)r; }
+};
 
 // NC = 1: one vector of n = N per CTA.  NC = 2: one vector of n = 2N per cluster pair (see header).
 template <typename P, bool kInv, int NC = 1>
@@ -406,9 +507,52 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   // inverse reads its inputs straight from it (no chunked H <-> HBM phase: two passes of shared
   // traffic fewer per vector); the cluster pair keeps them in H for the cross stage.
   constexpr bool kG3 = (NC == 1);
+  constexpr bool kST = (NC == 1 && P::kST && kInv);  // the staged forward measured slower (2 more barriers)
   const uint32_t k65536 = kTwo16;
+  T* SR = reinterpret_cast<T*>(H);  // kST: the staged natural-order row (aliases H)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + P::BAR_OFF);
   auto pass3 = [&](auto inv, T* xv) {
     constexpr bool kI = decltype(inv)::value;
+    if constexpr (kST) {
+      // set k = tid (tid 0: the zero-imaginary set k = 512 and the DC set); the staged row SR in place of
+      // the global one.  zr/zi carry the results across the barrier; tid 0 packs its DC set into the
+      // registers its half set leaves free (forward: zr/zi[M3/2 ..]; inverse: zi) so the live set across
+      // the barrier stays 2 M3 floats on every path.
+      using SIO = sio1<T>;
+      using SST = sst1<T>;
+      float zr[M3], zi[M3];
+      const int kk = tid;
+      if (kk == 0) {
+        float d[M3];
+        pl_set_in<P, M3, kI, OffP3<P>, true, true, SIO>(zr, zi, H + K3, H - K3, true, tw3_for(K3), SR + K3, SR - K3,
+                                                        1024, k65536);
+        pl_dc_g_in<P, M3, kI, OffP3<P>, SIO>(d, H, SR, 1024, k65536);
+        ct::static_for<0, M3>([&](auto J) {
+          constexpr int j = decltype(J)::value;
+          if constexpr (kI) zi[j] = d[j];
+          else if constexpr (j < M3 / 2) zr[M3 / 2 + j] = d[j];
+          else zi[j] = d[j];
+        });
+      } else {
+        pl_set_in<P, M3, kI, OffP3<P>, false, true, SIO>(zr, zi, H + kk, H - kk, false, tw3_for(kk), SR + kk,
+                                                         SR - kk, 1024, k65536);
+      }
+      __syncthreads();  // every set read: H / SR free for the writes
+      if (kk == 0) {
+        float d[M3];
+        ct::static_for<0, M3>([&](auto J) {
+          constexpr int j = decltype(J)::value;
+          if constexpr (kI) d[j] = zi[j];
+          else if constexpr (j < M3 / 2) d[j] = zr[M3 / 2 + j];
+          else d[j] = zi[j];
+        });
+        pl_set_out<P, M3, kI, OffP3<P>, true, true, SST>(zr, zi, H + K3, H - K3, true, SR + K3, SR - K3, 1024);
+        pl_dc_g_out<P, M3, kI, OffP3<P>, SST>(d, H, SR, 1024, kI ? 1.0f / N : 1.0f);
+      } else {
+        pl_set_out<P, M3, kI, OffP3<P>, false, true, SST>(zr, zi, H + kk, H - kk, false, SR + kk, SR - kk, 1024);
+      }
+      return;
+    }
 #pragma unroll 1
     for (int i = 0; i < P::K3PT; ++i) {
       const int kk = tid + NT * i;
@@ -435,8 +579,25 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   LTw2 tw2;
   tw2.h = TW2 + (k2 - 1);
   float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
+  if (kST && tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  // kST inverse: the row of vector vv -> SR (TMA bulk load; 4 copies of N/4 elements)
+  auto issue_row = [&](int64_t vv) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(bar, (uint32_t)(N * sizeof(T)));
+    ct::static_for<0, 4>([&](auto C) {
+      constexpr int c = decltype(C)::value;
+      bulk_g2s(SR + c * (N / 4), x + vv * NV + c * (N / 4), (uint32_t)(N / 4 * sizeof(T)), bar);
+    });
+  };
   __syncthreads();
   if constexpr (NC == 2) cooperative_groups::this_cluster().sync();  // peer's H mapped and live
+  if constexpr (kST && kInv) {
+    if (tid == 0 && (int64_t)blockIdx.x < batch) issue_row(blockIdx.x);
+  }
+  uint32_t it = 0;
   // bf16 forward, one vector per CTA: pass 1's element pairs of the NEXT vector are loaded into
   // registers (32 raw bf16x2 words per thread) right after this vector's pass 1, so their HBM latency
   // hides behind passes 2 and 3 instead of stalling the next pass 1
@@ -448,7 +609,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       ct::static_for<0, R>([&](auto I) { pf[decltype(I)::value] = __ldcs(src + (S / 2) * decltype(I)::value); });
     }
   }
-  for (int64_t v = blockIdx.x / NC; v < batch; v += gridDim.x / NC) {
+  const uint32_t psel = pair_ld<T>::sel(r);
+  for (int64_t v = blockIdx.x / NC; v < batch; v += gridDim.x / NC, ++it) {
     T* xv = x + v * NV;
     T* xh = xv + r;  // this CTA's half: elements xh[XS * e], e < N
     if (!kInv) {
@@ -461,9 +623,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
             b[rev_bits<5>(i)] = make_float2(__uint_as_float(pf[i] * k65536), __uint_as_float(pf[i] & 0xffff0000u));
           else if constexpr (NC == 1)
             b[rev_bits<5>(i)] = gio<T>::ld2(xv + 2 * c + S * i, k65536);
-          else
-            b[rev_bits<5>(i)] = make_float2(gio1<T>::ld(xh + XS * (2 * c + S * i), k65536),
-                                            gio1<T>::ld(xh + XS * (2 * c + 1 + S * i), k65536));
+          else  // x[r :: 2] at 2 (2c + S i) and 2 (2c + 1 + S i): the group of 4 at 4c + 2 S i
+            b[rev_bits<5>(i)] = pair_ld<T>::ld(xv + 4 * c + 2 * S * i, psel);
         });
         if constexpr (kPF) {
           const int64_t vn = v + gridDim.x;
@@ -473,6 +634,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
           }
         }
         rfft_fwd_reg<R>(b);
+        if constexpr (kST) {  // the previous vector's bulk store still reads SR (= H)
+          if (tid == 0) bulk_wait_read<0>();
+          __syncthreads();  // (kST: S / 2 == NT, every thread is here)
+        }
         const int w0 = rev_bits<P::LS>(2 * c), w1 = w0 + S / 2;
         float* h0 = H + P::phys(w0 * 32);  // a window never crosses a pad boundary
         float* h1 = H + P::phys(w1 * 32);
@@ -487,7 +652,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       if (act2 && k2 == 16) pl_dc<P, 32, false, OffP2<P>>(h2, 1.0f);
       __syncthreads();
       pass3(std::false_type{}, xv);
-      if constexpr (NC == 1) {
+      if constexpr (kST) {
+        fence_proxy_async_smem();  // SR's generic writes before the bulk store reads them
+        __syncthreads();
+        if (tid == 0) {
+          ct::static_for<0, 4>([&](auto C) {
+            constexpr int c = decltype(C)::value;
+            bulk_s2g(xv + c * (N / 4), SR + c * (N / 4), (uint32_t)(N / 4 * sizeof(T)));
+          });
+          bulk_commit();
+        }
+      } else if constexpr (NC == 1) {
         __syncthreads();  // H is read by pass 3 until here; the next vector's pass 1 writes it
       } else {
         cooperative_groups::this_cluster().sync();  // both windows complete and visible
@@ -499,7 +674,8 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         pl_cross_inv<P>(H0, H1, TWCa, twb, xv, r, tid, k65536);
         cooperative_groups::this_cluster().sync();  // both windows written (half of each remotely)
       }
-      pass3(std::true_type{}, xv);  // NC = 1: reads the row straight from HBM
+      if constexpr (kST) mbar_wait(bar, it & 1);  // this vector's row staged in SR
+      pass3(std::true_type{}, xv);  // NC = 1: reads the row straight from HBM (kST: from SR)
       __syncthreads();
       if (act2) pl_set<P, 32, true, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
       if (act2 && k2 == 16) pl_dc<P, 32, true, OffP2<P>>(h2, 1.0f);
@@ -519,6 +695,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
           b[i + 2] = make_float2(f0.z, f1.z);
           b[i + 3] = make_float2(f0.w, f1.w);
         });
+        if constexpr (kST) {  // H read: the next vector's row may land in SR (= H)
+          __syncthreads();
+          if (tid == 0 && v + gridDim.x < batch) issue_row(v + gridDim.x);
+        }
         rfft_inv_reg<R>(b);
         ct::static_for<0, R>([&](auto I) {
           constexpr int i = decltype(I)::value;
@@ -530,11 +710,18 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
           }
         });
       }
-      if constexpr (NC == 1)
+      if constexpr (kST) {
+        // no barrier: H was released after pass 1's reads, and the next vector's pass 3 writes H only
+        // after its own barrier
+      } else if constexpr (NC == 1) {
         __syncthreads();
-      else
+      } else {
         cooperative_groups::this_cluster().sync();  // the peer's next cross stage writes this H
+      }
     }
+  }
+  if constexpr (kST && !kInv) {
+    if (tid == 0) bulk_wait<0>();
   }
 }
 
