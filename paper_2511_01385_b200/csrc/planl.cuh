@@ -63,7 +63,7 @@ struct PlanL {
   // writes) — the forward's outputs leave through TMA bulk stores, the inverse's inputs arrive by a TMA
   // bulk load issued as soon as the previous vector's pass 1 has read H — instead of one 2-byte
   // global access per slot (lg_throttle-bound at one CTA per SM).  mbarrier at BAR_OFF.
-  static constexpr bool kST = (K3PT == 1);
+  static constexpr bool kST = (K3PT * M3 <= 32);  // all of a thread's pass-3 sets fit in 64 registers
   static constexpr size_t BAR_OFF = BYTES1;
   static constexpr size_t BYTES = BYTES1 + 16;
   static_assert((size_t)N * sizeof(T) <= (size_t)N * 4, "the staged row fits in H");
@@ -507,50 +507,61 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   // inverse reads its inputs straight from it (no chunked H <-> HBM phase: two passes of shared
   // traffic fewer per vector); the cluster pair keeps them in H for the cross stage.
   constexpr bool kG3 = (NC == 1);
-  constexpr bool kST = (NC == 1 && P::kST && kInv);  // the staged forward measured slower (2 more barriers)
+  // the staged forward costs 2 more barriers per vector: slower at one CTA per SM (n = 32768)
+  constexpr bool kST = (NC == 1 && P::kST && (kInv || P::MINB > 1));
   const uint32_t k65536 = kTwo16;
   T* SR = reinterpret_cast<T*>(H);  // kST: the staged natural-order row (aliases H)
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + P::BAR_OFF);
   auto pass3 = [&](auto inv, T* xv) {
     constexpr bool kI = decltype(inv)::value;
     if constexpr (kST) {
-      // set k = tid (tid 0: the zero-imaginary set k = 512 and the DC set); the staged row SR in place of
-      // the global one.  zr/zi carry the results across the barrier; tid 0 packs its DC set into the
-      // registers its half set leaves free (forward: zr/zi[M3/2 ..]; inverse: zi) so the live set across
-      // the barrier stays 2 M3 floats on every path.
+      // sets k = tid + NT i, i < K3PT (tid 0, i = 0: the zero-imaginary set k = 512 and the DC set); the
+      // staged row SR in place of the global one.  zr/zi carry the results across the barrier; tid 0
+      // packs its DC set into the registers its half set leaves free (forward: zr/zi[M3/2 ..]; inverse:
+      // zi) so the live set across the barrier stays 2 K3PT M3 floats on every path.
       using SIO = sio1<T>;
       using SST = sst1<T>;
-      float zr[M3], zi[M3];
-      const int kk = tid;
-      if (kk == 0) {
-        float d[M3];
-        pl_set_in<P, M3, kI, OffP3<P>, true, true, SIO>(zr, zi, H + K3, H - K3, true, tw3_for(K3), SR + K3, SR - K3,
-                                                        1024, k65536);
-        pl_dc_g_in<P, M3, kI, OffP3<P>, SIO>(d, H, SR, 1024, k65536);
-        ct::static_for<0, M3>([&](auto J) {
-          constexpr int j = decltype(J)::value;
-          if constexpr (kI) zi[j] = d[j];
-          else if constexpr (j < M3 / 2) zr[M3 / 2 + j] = d[j];
-          else zi[j] = d[j];
-        });
-      } else {
-        pl_set_in<P, M3, kI, OffP3<P>, false, true, SIO>(zr, zi, H + kk, H - kk, false, tw3_for(kk), SR + kk,
-                                                         SR - kk, 1024, k65536);
-      }
+      constexpr int KP = P::K3PT;
+      float zr[KP][M3], zi[KP][M3];
+      ct::static_for<0, KP>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int kk = tid + NT * i;
+        if (i == 0 && kk == 0) {
+          float d[M3];
+          pl_set_in<P, M3, kI, OffP3<P>, true, true, SIO>(zr[i], zi[i], H + K3, H - K3, true, tw3_for(K3), SR + K3,
+                                                          SR - K3, 1024, k65536);
+          pl_dc_g_in<P, M3, kI, OffP3<P>, SIO>(d, H, SR, 1024, k65536);
+          ct::static_for<0, M3>([&](auto J) {
+            constexpr int j = decltype(J)::value;
+            if constexpr (kI) zi[i][j] = d[j];
+            else if constexpr (j < M3 / 2) zr[i][M3 / 2 + j] = d[j];
+            else zi[i][j] = d[j];
+          });
+        } else {
+          pl_set_in<P, M3, kI, OffP3<P>, false, true, SIO>(zr[i], zi[i], H + kk, H - kk, false, tw3_for(kk),
+                                                           SR + kk, SR - kk, 1024, k65536);
+        }
+      });
       __syncthreads();  // every set read: H / SR free for the writes
-      if (kk == 0) {
-        float d[M3];
-        ct::static_for<0, M3>([&](auto J) {
-          constexpr int j = decltype(J)::value;
-          if constexpr (kI) d[j] = zi[j];
-          else if constexpr (j < M3 / 2) d[j] = zr[M3 / 2 + j];
-          else d[j] = zi[j];
-        });
-        pl_set_out<P, M3, kI, OffP3<P>, true, true, SST>(zr, zi, H + K3, H - K3, true, SR + K3, SR - K3, 1024);
-        pl_dc_g_out<P, M3, kI, OffP3<P>, SST>(d, H, SR, 1024, kI ? 1.0f / N : 1.0f);
-      } else {
-        pl_set_out<P, M3, kI, OffP3<P>, false, true, SST>(zr, zi, H + kk, H - kk, false, SR + kk, SR - kk, 1024);
-      }
+      ct::static_for<0, KP>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        const int kk = tid + NT * i;
+        if (i == 0 && kk == 0) {
+          float d[M3];
+          ct::static_for<0, M3>([&](auto J) {
+            constexpr int j = decltype(J)::value;
+            if constexpr (kI) d[j] = zi[i][j];
+            else if constexpr (j < M3 / 2) d[j] = zr[i][M3 / 2 + j];
+            else d[j] = zi[i][j];
+          });
+          pl_set_out<P, M3, kI, OffP3<P>, true, true, SST>(zr[i], zi[i], H + K3, H - K3, true, SR + K3, SR - K3,
+                                                           1024);
+          pl_dc_g_out<P, M3, kI, OffP3<P>, SST>(d, H, SR, 1024, kI ? 1.0f / N : 1.0f);
+        } else {
+          pl_set_out<P, M3, kI, OffP3<P>, false, true, SST>(zr[i], zi[i], H + kk, H - kk, false, SR + kk, SR - kk,
+                                                            1024);
+        }
+      });
       return;
     }
 #pragma unroll 1
