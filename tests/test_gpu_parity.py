@@ -204,9 +204,11 @@ NL = [8192, 16384, 32768]
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("n", NL)
 def test_large_n_forward_inverse(n, dtype):
-    """One vector per CTA: a batch above the grid (persistent loop) with sampled rows against the
-    oracle (forward and inverse), the round trip on every row, and exact placement probes."""
-    b = 2 * 148 + 7
+    """One vector per CTA: a batch above the grid at every n (up to 4 CTAs per SM at n = 8192: the
+    persistent loop, the staged row's TMA re-issue and its mbarrier phase flip) with sampled rows
+    against the oracle (forward and inverse; the last row is a CTA's second vector), the round trip
+    on every row, and exact placement probes."""
+    b = 4 * 148 + 7
     x = synth.randn((b, n), seed=700 + n, dtype=dtype).cuda()
     x[0].zero_()
     x[0, 0] = 1  # impulse -> exactly ones in slots 0 .. n/2, zeros elsewhere (P2)

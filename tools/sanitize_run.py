@@ -3,7 +3,8 @@
   compute-sanitizer --tool racecheck python tools/sanitize_run.py
 Transforms n = 2 .. 65536 (plan2, plan2o, plan3, planl, cluster pair), packed products, utilities,
 BCA forward / accumulate / backward on the fused (p = 256, 512, 1024, 2048, 4096), resident-spectra
-and tiled kernels, both dtypes.  Sizes are small: the point is coverage, not speed."""
+and tiled kernels, both dtypes.  Sizes are small: the point is coverage, not speed ("large": the large-n
+plans with more vectors than CTAs)."""
 import os
 import sys
 
@@ -26,6 +27,13 @@ for dt in ("bf16", "f32"):
             if n <= 4096:
                 c = R.rdfft_decode(x)
                 R.rdfft_encode(c, x)
+        torch.cuda.synchronize()
+    if only == "large":  # the large-n plans with more vectors than CTAs (the persistent loop, the staged
+        # row's TMA re-issue and mbarrier phase flip; n = 65536: more pairs than the grid holds)
+        for n, b in ((8192, 600), (16384, 300), (32768, 150), (65536, 80)):
+            x = synth.randn((b, n), seed=n, dtype=dt, device="cuda")
+            R.rdfft_fwd(x)
+            R.rdfft_inv(x)
         torch.cuda.synchronize()
     if only in ("all", "bca", "bca_synccheck"):
         for (qo, qi, p, T) in ((4, 4, 1024, 9), (3, 3, 256, 11), (2, 2, 512, 7), (1, 1, 2048, 9), (2, 2, 2048, 5),
