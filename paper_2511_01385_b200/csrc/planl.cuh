@@ -49,7 +49,7 @@ struct PlanL {
   static constexpr int K3PT = K3 / NT;
   static constexpr int MINB = 512 / NT;  // CTAs per SM the 128-register budget allows
   static_assert(S / 2 == NW2 * 16 || NT == 512, "pass-2 sets per thread");
-  static constexpr int TW2N = 32 * 16, TW3N = (M3 / 4) * K3;
+  static constexpr int TW2N = 32 * 17, TW3N = (M3 / 4) * K3;
   static constexpr int HPAD = 64;  // additive pad: 4 floats per n/16 slots (see phys)
   static constexpr size_t TW2_OFF = (size_t)(N + HPAD) * 4;
   static constexpr size_t TW3_OFF = TW2_OFF + (size_t)TW2N * 8;
@@ -120,11 +120,19 @@ struct LTw3 {
 // LD = gio1<T>) or the staged row in shared memory (ST = sst1<T>, LD = sio1<T>; PlanL::kST).
 // Split in two phases so the staged pass 3 can put a barrier between them: pl_set_in reads the set
 // and runs its arithmetic into (zr, zi), pl_set_out writes the results.
+struct NoFix {
+  template <int M>
+  __device__ __forceinline__ void operator()(float (&)[M], float (&)[M]) const {}
+};
+
+// fix(zr, zi) runs right after the loads (before the forward's twiddles / the inverse's DIT): pass 2's
+// paired block-DC / block-Nyquist sets (PairFix below) hook in there.
 template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false,
-          typename LD = gio1<typename P::elem>, typename TW>
+          typename LD = gio1<typename P::elem>, typename TW, typename FIX = NoFix>
 __device__ __forceinline__ void pl_set_in(float (&zr)[M], float (&zi)[M], float* pa, float* pb, bool half,
                                           const TW& tw, const typename P::elem* ga = nullptr,
-                                          const typename P::elem* gb = nullptr, int m0 = 0, uint32_t k65536 = 0) {
+                                          const typename P::elem* gb = nullptr, int m0 = 0, uint32_t k65536 = 0,
+                                          const FIX& fix = FIX{}) {
   constexpr int LM = ilog2c<M>();
   auto A = [&](auto J) -> float& {
     constexpr int j = decltype(J)::value;
@@ -142,6 +150,7 @@ __device__ __forceinline__ void pl_set_in(float (&zr)[M], float (&zi)[M], float*
       if constexpr (kHalfB) zi[j] = 0.f;
       else zi[j] = half ? 0.f : B(J);
     });
+    fix(zr, zi);
     ct::static_for<1, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
       const float2 t = tw.template at<rev_bits<LM>(j)>();
@@ -184,6 +193,7 @@ __device__ __forceinline__ void pl_set_in(float (&zr)[M], float (&zi)[M], float*
         }
       }
     });
+    fix(zr, zi);
     cfft_dit<M, true>(zr, zi);
     ct::static_for<0, M>([&](auto J) {
       constexpr int j = decltype(J)::value;
@@ -306,34 +316,109 @@ __device__ __forceinline__ void pl_dc(float* p0, float scale) {
   });
 }
 
-// pass-2 twiddle: TW2[j][k-1] = W_1024^{k rev5(j)} (conj for the inverse), indexed by natural j
+// pass-2 twiddle: TW2[j][c] (17 columns), indexed by natural j: c = k - 1 (k = 1 .. 15) W_1024^{k rev5(j)};
+// c = 15 the paired block-Nyquist sets (k = 16), c = 16 the paired block-DC sets (k = 0, no twiddle).
+// Forward: the paired columns carry the factor 1/2 of the two-for-one split (PairFix); inverse: conj.
 struct LTw2 {
-  const float2* h;  // &TW2[0][k-1]
+  static constexpr int kStride = 17;
+  const float2* h;  // &TW2[0][c]
   template <int R_>
   __device__ __forceinline__ float2 at() const {
-    return h[rev_bits<5>(R_) * 16];
+    return h[rev_bits<5>(R_) * kStride];
   }
 };
 
-template <typename T>
-struct gio4;  // 4 consecutive elements <-> float4
-template <>
-struct gio4<float> {
-  __device__ __forceinline__ static float4 ld(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
-  __device__ __forceinline__ static void st(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
-};
-template <>
-struct gio4<__nv_bfloat16> {
-  __device__ __forceinline__ static float4 ld(const __nv_bfloat16* p) {
-    const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));
-    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u), __uint_as_float(u.y << 16),
-                       __uint_as_float(u.y & 0xffff0000u));
+// Pass 2, paired sets (round 2): each 1024-slot window has 15 complex sets (k = 1 .. 15), a real-input
+// set of its block Nyquists (k = 16) and a real one of its block DCs (k = 0).  Instead of one lane per
+// window running the k = 16 set with a zero imaginary part AND then the DC set as a real FFT (1.5 sets
+// of instructions for its whole warp), two windows w1, w2 share one complex 32-point set per kind:
+// z = (s1 + i s2) (the twiddle is a scalar, so it applies to the sum), then the two spectra separate by
+// symmetry — the DC sets' outputs satisfy X[-q] = conj X[q], the Nyquist sets' U[31 - q] = conj U[q]
+// (bins 32 q + 16 of a real 1024-point spectrum).  Every lane then runs exactly one complex set; the
+// pair's loads and stores are the regular set code with pa = window w1, pb = window w2 (rebased), and
+// only this fix-up differs.  R(q) below = the registers of DFT index q (inverse: at position rev5(q)).
+template <int M, bool kInv>
+struct PairFix {
+  int kind;  // 0: regular set (no-op), 1: paired DC sets, 2: paired Nyquist (k = 16) sets
+  float s0;  // forward: scale of the j = 0 input (1/2 for the pairs; the table carries it for j >= 1)
+  __device__ __forceinline__ void operator()(float (&zr)[M], float (&zi)[M]) const {
+    static_assert(M == 32, "pass-2 sets");
+    if constexpr (!kInv) {
+      zr[0] *= s0;  // (uniform: every lane, s0 = 1 for the regular sets)
+      zi[0] *= s0;
+    } else if (kind == 1) {
+      // loaded: R(q) = (P1[q], P2[31-q]) for q < 16, (P2[31-q], -P1[q]) for q >= 16 (P1 / P2 = the two
+      // windows' packed DC spectra); wanted: R(q) = Z_q = X1_q + i X2_q.
+      float nr[M], ni[M];
+      nr[0] = zr[rev_bits<5>(0)];
+      ni[0] = zr[rev_bits<5>(31)];  // Z_0 = P1[0] + i P2[0]
+      nr[16] = -zi[rev_bits<5>(16)];
+      ni[16] = zi[rev_bits<5>(15)];  // Z_16 = P1[16] + i P2[16]
+      ct::static_for<1, 16>([&](auto Q) {
+        constexpr int q = decltype(Q)::value, r = 32 - q;
+        const float p1q = zr[rev_bits<5>(q)], p1r = -zi[rev_bits<5>(r)];
+        const float p2r = zi[rev_bits<5>(q - 1)], p2q = zr[rev_bits<5>(31 - q)];
+        nr[q] = p1q - p2r;
+        ni[q] = p1r + p2q;
+        nr[r] = p1q + p2r;
+        ni[r] = p2q - p1r;
+      });
+      ct::static_for<0, M>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        zr[rev_bits<5>(q)] = nr[q];
+        zi[rev_bits<5>(q)] = ni[q];
+      });
+    } else if (kind == 2) {
+      // loaded: R(q) = (Re U1_q, Im U2_q), R(31-q) = (Re U2_q, -Im U1_q) for q < 16; wanted Z = U1 + i U2
+      ct::static_for<0, 16>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        constexpr int a = rev_bits<5>(q), b = rev_bits<5>(31 - q);
+        const float u1r = zr[a], u2i = zi[a], u2r = zr[b], mu1i = zi[b];
+        zr[a] = u1r - u2i;
+        zi[a] = u2r - mu1i;
+        zr[b] = u1r + u2i;
+        zi[b] = u2r + mu1i;
+      });
+    }
   }
-  __device__ __forceinline__ static void st(__nv_bfloat16* p, float4 v) {
-    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
-    __stcs(reinterpret_cast<uint2*>(p), make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b)));
-  }
 };
+
+// Forward pass 2, paired Nyquist sets: Z (natural order, the 1/2 already in) -> in place, the registers
+// the regular store code (pl_set_out) writes to the two windows: window 1 slot 32 t + 16 <- (t < 16 ? zr[t]
+// : -zi[t]), window 2 slot 32 (31 - t) + 16 <- (t < 16 ? zi[t] : zr[t]).  U1 = Z_q + conj Z_{31-q},
+// U2 = -i (Z_q - conj Z_{31-q}); each q < 16 pair maps onto its own four registers.
+template <int M>
+__device__ __forceinline__ void pair_nyq_fwd_out(float (&zr)[M], float (&zi)[M]) {
+  static_assert(M == 32, "pass-2 sets");
+  ct::static_for<0, 16>([&](auto Q) {
+    constexpr int q = decltype(Q)::value, r = 31 - q;
+    const float ar = zr[q], ai = zi[q], br = zr[r], bi = zi[r];
+    zr[q] = ar + br;  // Re U1_q
+    zi[q] = br - ar;  // Im U2_q
+    zi[r] = bi - ai;  // -Im U1_q
+    zr[r] = ai + bi;  // Re U2_q
+  });
+}
+// Forward pass 2, paired DC sets: X1 = Z_q + conj Z_{-q}, X2 = -i (Z_q - conj Z_{-q}) stored as the two
+// windows' packed real 32-point spectra (slot 32 s of window w at hw + OffP2::a(s)); its own stores (the
+// regular store order would need a register permutation, which spilled next to the bf16 prefetch).
+template <typename P, int M>
+__device__ __forceinline__ void pair_dc_fwd_store(const float (&zr)[M], const float (&zi)[M], float* hw1,
+                                                  float* hw2) {
+  static_assert(M == 32, "pass-2 sets");
+  using OFF = OffP2<P>;
+  hw1[OFF::a(0)] = zr[0] + zr[0];
+  hw2[OFF::a(0)] = zi[0] + zi[0];
+  hw1[OFF::a(16)] = zr[16] + zr[16];
+  hw2[OFF::a(16)] = zi[16] + zi[16];
+  ct::static_for<1, 16>([&](auto Q) {
+    constexpr int q = decltype(Q)::value, r = 32 - q;
+    hw1[OFF::a(q)] = zr[q] + zr[r];  // Re X1_q
+    hw1[OFF::a(r)] = zi[q] - zi[r];  // Im X1_q
+    hw2[OFF::a(q)] = zi[q] + zi[r];  // Re X2_q
+    hw2[OFF::a(r)] = zr[r] - zr[q];  // Im X2_q
+  });
+}
 
 // Cluster-pair cross stage (m = N, the vector has 2N slots), forward: groups k in this CTA's
 // quarter, A from window 0 (H0), B from window 1 (H1), outputs straight to the global row xv.
@@ -478,11 +563,17 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   float* H1 = r == 0 ? Hpeer : H;
   constexpr int64_t NV = (int64_t)N * NC;  // elements per vector
   constexpr int XS = NC;                   // element stride of this CTA's half in the row
-  for (int e = tid; e < P::TW2N; e += NT) {
-    const int j = e / 16, k = 1 + e % 16;
+  // pass 2 with paired DC / Nyquist sets (PairFix): measured faster for n <= 16384 except the bf16
+  // forward, whose next-vector prefetch registers it would displace (the divergent fix-up spilled next to
+  // them); slower at n = 32768 (one CTA per SM: r02_v21)
+  constexpr bool kPair = (N <= 16384 && (kInv || sizeof(T) == 4));
+  for (int e = tid; e < P::TW2N; e += NT) {  // LTw2's 17 columns (the paired ones: 1/2 in the forward)
+    const int j = e / LTw2::kStride, col = e % LTw2::kStride;
+    const int k = col == 16 ? 0 : col + 1;
+    const float h = (!kInv && kPair && col >= 15) ? 0.5f : 1.0f;
     float s, c;
     sincospif(2.0f * (float)(k * rev_bits<5>(j)) / 1024.0f, &s, &c);
-    TW2[e] = make_float2(c, sg * s);
+    TW2[e] = make_float2(h * c, h * sg * s);
   }
   for (int e = tid; e < P::TW3N; e += NT) {
     const int a = e / K3, k = 1 + e % K3;
@@ -585,11 +676,27 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   // adjacent blocks they overlapped: 2-way conflicts on every pass-2 access).
   constexpr int D2 = N / 4096;
   const int w32 = tid / 32, hw = (tid / 16) & 1;
-  const int ww = (w32 % D2) + (w32 / D2) * 2 * D2 + hw * D2, k2 = tid % 16 == 0 ? 16 : tid % 16;
+  const int ww = (w32 % D2) + (w32 / D2) * 2 * D2 + hw * D2, k2 = (kPair || tid % 16 != 0) ? tid % 16 : 16;
   const bool act2 = tid < P::NW2 * 16;
+  float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
+  // lanes k2 = 1 .. 15: set k2 of window ww; lane k2 = 0 of each half-warp: a paired set (PairFix) of the
+  // warp's two windows w1 = ww(hw 0), w2 = w1 + D2 — block DCs on half-warp 0, block Nyquists on half-warp
+  // 1.  Their slots 32 j (+ 16) then fall on the two banks the 30 regular lanes leave free (the half-warps'
+  // pads differ by 16 floats): a pairing across other windows put a 2-way conflict on every pass-2 access.
+  // (!kPair: lane 0 of a half-warp runs its window's k = 16 set with a zero imaginary part, then its DC set)
+  const int pkind = (!kPair || k2 != 0) ? 0 : (hw == 0 ? 1 : 2);
+  float* pa2 = h2 + k2;
+  float* pb2 = h2 - k2;
   LTw2 tw2;
   tw2.h = TW2 + (k2 - 1);
-  float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
+  if (pkind != 0) {
+    float* hw1 = H + P::phys((ww - hw * D2) * 1024);
+    float* hw2 = H + P::phys((ww - hw * D2 + D2) * 1024);
+    pa2 = pkind == 1 ? hw1 : hw1 + 16;       // A(j): window 1 slot 32 j (+ 16)
+    pb2 = pkind == 1 ? hw2 - 32 : hw2 - 16;  // B(j) = pb[32 (j + 1)]: window 2 slot 32 j (+ 16)
+    tw2.h = TW2 + (pkind == 1 ? 16 : 15);
+  }
+  const PairFix<32, kInv> pfix{pkind, pkind != 0 ? 0.5f : 1.0f};
   if (kST && tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -659,8 +766,21 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         });
       }
       __syncthreads();
-      if (act2) pl_set<P, 32, false, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
-      if (act2 && k2 == 16) pl_dc<P, 32, false, OffP2<P>>(h2, 1.0f);
+      if constexpr (kPair) {
+        if (act2) {
+          float zr[32], zi[32];
+          pl_set_in<P, 32, false, OffP2<P>>(zr, zi, pa2, pb2, false, tw2, nullptr, nullptr, 0, 0u, pfix);
+          if (pkind == 1) {
+            pair_dc_fwd_store<P>(zr, zi, pa2, pb2 + 32);
+          } else {
+            if (pkind == 2) pair_nyq_fwd_out(zr, zi);
+            pl_set_out<P, 32, false, OffP2<P>>(zr, zi, pa2, pb2, false);
+          }
+        }
+      } else {
+        if (act2) pl_set<P, 32, false, OffP2<P>>(pa2, pb2, k2 == 16, tw2);
+        if (act2 && k2 == 16) pl_dc<P, 32, false, OffP2<P>>(h2, 1.0f);
+      }
       __syncthreads();
       pass3(std::false_type{}, xv);
       if constexpr (kST) {
@@ -688,8 +808,16 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       if constexpr (kST) mbar_wait(bar, it & 1);  // this vector's row staged in SR
       pass3(std::true_type{}, xv);  // NC = 1: reads the row straight from HBM (kST: from SR)
       __syncthreads();
-      if (act2) pl_set<P, 32, true, OffP2<P>>(h2 + k2, h2 - k2, k2 == 16, tw2);
-      if (act2 && k2 == 16) pl_dc<P, 32, true, OffP2<P>>(h2, 1.0f);
+      if constexpr (kPair) {
+        if (act2) {
+          float zr[32], zi[32];
+          pl_set_in<P, 32, true, OffP2<P>>(zr, zi, pa2, pb2, false, tw2, nullptr, nullptr, 0, 0u, pfix);
+          pl_set_out<P, 32, true, OffP2<P>>(zr, zi, pa2, pb2, false);
+        }
+      } else {
+        if (act2) pl_set<P, 32, true, OffP2<P>>(pa2, pb2, k2 == 16, tw2);
+        if (act2 && k2 == 16) pl_dc<P, 32, true, OffP2<P>>(h2, 1.0f);
+      }
       __syncthreads();
       if (tid < S / 2) {  // inverse pass 1
         const int c = tid;
