@@ -339,25 +339,33 @@ struct LTw2 {
 // only this fix-up differs.  R(q) below = the registers of DFT index q (inverse: at position rev5(q)).
 template <int M, bool kInv>
 struct PairFix {
-  int kind;  // 0: regular set (no-op), 1: paired DC sets, 2: paired Nyquist (k = 16) sets
-  float s0;  // forward: scale of the j = 0 input (1/2 for the pairs; the table carries it for j >= 1)
+  int kind;   // 0: regular set (no-op), 1: paired DC sets, 2: paired Nyquist sets
+  float s0;   // forward: scale of the j = 0 input (1/2 for the pairs; the table carries it for j >= 1)
+  bool has1;  // inverse: the second set exists (a ragged tile's last pair may have one member only)
   __device__ __forceinline__ void operator()(float (&zr)[M], float (&zi)[M]) const {
-    static_assert(M == 32, "pass-2 sets");
+    constexpr int LM = ilog2c<M>(), H = M / 2;
     if constexpr (!kInv) {
       zr[0] *= s0;  // (uniform: every lane, s0 = 1 for the regular sets)
       zi[0] *= s0;
     } else if (kind == 1) {
-      // loaded: R(q) = (P1[q], P2[31-q]) for q < 16, (P2[31-q], -P1[q]) for q >= 16 (P1 / P2 = the two
-      // windows' packed DC spectra); wanted: R(q) = Z_q = X1_q + i X2_q.
+      // loaded: R(q) = (P1[q], P2[M-1-q]) for q < M/2, (P2[M-1-q], -P1[q]) for q >= M/2 (P1 / P2 = the
+      // two packed real DC spectra); wanted: R(q) = Z_q = X1_q + i X2_q.
+      if (!has1) {
+        ct::static_for<0, H>([&](auto Q) {
+          constexpr int q = decltype(Q)::value;
+          zi[rev_bits<LM>(q)] = 0.f;
+          zr[rev_bits<LM>(q + H)] = 0.f;
+        });
+      }
       float nr[M], ni[M];
-      nr[0] = zr[rev_bits<5>(0)];
-      ni[0] = zr[rev_bits<5>(31)];  // Z_0 = P1[0] + i P2[0]
-      nr[16] = -zi[rev_bits<5>(16)];
-      ni[16] = zi[rev_bits<5>(15)];  // Z_16 = P1[16] + i P2[16]
-      ct::static_for<1, 16>([&](auto Q) {
-        constexpr int q = decltype(Q)::value, r = 32 - q;
-        const float p1q = zr[rev_bits<5>(q)], p1r = -zi[rev_bits<5>(r)];
-        const float p2r = zi[rev_bits<5>(q - 1)], p2q = zr[rev_bits<5>(31 - q)];
+      nr[0] = zr[rev_bits<LM>(0)];
+      ni[0] = zr[rev_bits<LM>(M - 1)];  // Z_0 = P1[0] + i P2[0]
+      nr[H] = -zi[rev_bits<LM>(H)];
+      ni[H] = zi[rev_bits<LM>(H - 1)];  // Z_{M/2} = P1[M/2] + i P2[M/2]
+      ct::static_for<1, H>([&](auto Q) {
+        constexpr int q = decltype(Q)::value, r = M - q;
+        const float p1q = zr[rev_bits<LM>(q)], p1r = -zi[rev_bits<LM>(r)];
+        const float p2r = zi[rev_bits<LM>(q - 1)], p2q = zr[rev_bits<LM>(M - 1 - q)];
         nr[q] = p1q - p2r;
         ni[q] = p1r + p2q;
         nr[r] = p1q + p2r;
@@ -365,19 +373,21 @@ struct PairFix {
       });
       ct::static_for<0, M>([&](auto Q) {
         constexpr int q = decltype(Q)::value;
-        zr[rev_bits<5>(q)] = nr[q];
-        zi[rev_bits<5>(q)] = ni[q];
+        zr[rev_bits<LM>(q)] = nr[q];
+        zi[rev_bits<LM>(q)] = ni[q];
       });
     } else if (kind == 2) {
-      // loaded: R(q) = (Re U1_q, Im U2_q), R(31-q) = (Re U2_q, -Im U1_q) for q < 16; wanted Z = U1 + i U2
-      ct::static_for<0, 16>([&](auto Q) {
+      // loaded: R(q) = (Re U1_q, Im U2_q), R(M-1-q) = (Re U2_q, -Im U1_q) for q < M/2; wanted Z = U1 + i U2
+      ct::static_for<0, H>([&](auto Q) {
         constexpr int q = decltype(Q)::value;
-        constexpr int a = rev_bits<5>(q), b = rev_bits<5>(31 - q);
-        const float u1r = zr[a], u2i = zi[a], u2r = zr[b], mu1i = zi[b];
+        constexpr int a = rev_bits<LM>(q), b = rev_bits<LM>(M - 1 - q);
+        const float u1r = zr[a], u2r = zr[b], mu1i = zi[b];
+        const float u2i = has1 ? zi[a] : 0.f;
+        const float u2r_ = has1 ? u2r : 0.f;
         zr[a] = u1r - u2i;
-        zi[a] = u2r - mu1i;
+        zi[a] = u2r_ - mu1i;
         zr[b] = u1r + u2i;
-        zi[b] = u2r + mu1i;
+        zi[b] = u2r_ + mu1i;
       });
     }
   }
@@ -696,7 +706,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
     pb2 = pkind == 1 ? hw2 - 32 : hw2 - 16;  // B(j) = pb[32 (j + 1)]: window 2 slot 32 j (+ 16)
     tw2.h = TW2 + (pkind == 1 ? 16 : 15);
   }
-  const PairFix<32, kInv> pfix{pkind, pkind != 0 ? 0.5f : 1.0f};
+  const PairFix<32, kInv> pfix{pkind, pkind != 0 ? 0.5f : 1.0f, true};
   if (kST && tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
