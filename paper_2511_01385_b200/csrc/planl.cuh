@@ -456,22 +456,24 @@ __device__ __forceinline__ void pl_cross_fwd(const float* H0, const float* H1, c
     });
     ct::static_for<0, U>([&](auto I) {
       constexpr int u = decltype(I)::value;
+      // no branch in the batch (its reconvergence showed in the stall samples): k = 0 runs the group
+      // formula on k = m/2's slots (the loads above) and is overwritten after the loop
       const int k = r * Q + tid + NT * (i0 + u);
-      if (k == 0) {  // k = 0: (a, b) -> (a + b, a - b); k = m/2: slot m/2 kept, slot 3m/2 negated
-        const float a = H0[P::phys(0)], b = H1[P::phys(0)];
-        gio<T>::st1(xv, a + b);
-        gio<T>::st1(xv + m, a - b);
-        gio<T>::st1(xv + m / 2, H0[P::phys(m / 2)]);
-        gio<T>::st1(xv + 3 * m / 2, -H1[P::phys(m / 2)]);
-      } else {
-        const float wr = ta[u].x * twb.x - ta[u].y * twb.y, wi = ta[u].x * twb.y + ta[u].y * twb.x;
-        const float ur = fmaf(br[u], wr, -bi[u] * wi), ui = fmaf(br[u], wi, bi[u] * wr);
-        gio<T>::st1(xv + k, ar[u] + ur);
-        gio<T>::st1(xv + 2 * m - k, ai[u] + ui);
-        gio<T>::st1(xv + m - k, ar[u] - ur);
-        gio<T>::st1(xv + m + k, ui - ai[u]);
-      }
+      const int kk = k == 0 ? m / 2 : k;
+      const float wr = ta[u].x * twb.x - ta[u].y * twb.y, wi = ta[u].x * twb.y + ta[u].y * twb.x;
+      const float ur = fmaf(br[u], wr, -bi[u] * wi), ui = fmaf(br[u], wi, bi[u] * wr);
+      gio<T>::st1(xv + kk, ar[u] + ur);
+      gio<T>::st1(xv + 2 * m - kk, ai[u] + ui);
+      gio<T>::st1(xv + m - kk, ar[u] - ur);
+      gio<T>::st1(xv + m + kk, ui - ai[u]);
     });
+  }
+  if (r == 0 && tid == 0) {  // k = 0: (a, b) -> (a + b, a - b); k = m/2: slot m/2 kept, slot 3m/2 negated
+    const float a = H0[P::phys(0)], b = H1[P::phys(0)];
+    gio<T>::st1(xv, a + b);
+    gio<T>::st1(xv + m, a - b);
+    gio<T>::st1(xv + m / 2, H0[P::phys(m / 2)]);
+    gio<T>::st1(xv + 3 * m / 2, -H1[P::phys(m / 2)]);
   }
 }
 
@@ -497,23 +499,24 @@ __device__ __forceinline__ void pl_cross_inv(float* H0, float* H1, const float2*
     });
     ct::static_for<0, U>([&](auto I) {
       constexpr int u = decltype(I)::value;
+      // no branch in the batch: k = 0 runs the group formula on k = m/2's slots and is fixed up after
       const int k = r * Q + tid + NT * (i0 + u);
-      if (k == 0) {
-        const float s = gio1<T>::ld(xv, k65536), d = gio1<T>::ld(xv + m, k65536);
-        H0[P::phys(0)] = 0.5f * (s + d);
-        H1[P::phys(0)] = 0.5f * (s - d);
-        H0[P::phys(m / 2)] = ykr[u];   // slot m/2
-        H1[P::phys(m / 2)] = -yki[u];  // -(slot 3m/2)
-      } else {
-        const float2 ta = TWCa[k >> 7];  // conj(W_{2m}^k)
-        const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
-        const float dr = 0.5f * (ykr[u] - ymr[u]), di = 0.5f * (yki[u] - ymi[u]);
-        H0[P::phys(k)] = 0.5f * (ykr[u] + ymr[u]);
-        H0[P::phys(m - k)] = 0.5f * (yki[u] + ymi[u]);
-        H1[P::phys(k)] = fmaf(dr, wr, -di * wi);
-        H1[P::phys(m - k)] = fmaf(dr, wi, di * wr);
-      }
+      const int kk = k == 0 ? m / 2 : k;
+      const float2 ta = TWCa[kk >> 7];  // conj(W_{2m}^k)
+      const float wr = ta.x * twb.x - ta.y * twb.y, wi = ta.x * twb.y + ta.y * twb.x;
+      const float dr = 0.5f * (ykr[u] - ymr[u]), di = 0.5f * (yki[u] - ymi[u]);
+      H0[P::phys(kk)] = 0.5f * (ykr[u] + ymr[u]);
+      H0[P::phys(m - kk)] = 0.5f * (yki[u] + ymi[u]);
+      H1[P::phys(kk)] = fmaf(dr, wr, -di * wi);
+      H1[P::phys(m - kk)] = fmaf(dr, wi, di * wr);
     });
+  }
+  if (r == 0 && tid == 0) {  // k = 0 (slots 0, m) and the unpaired slots m/2, 3m/2
+    const float s = gio1<T>::ld(xv, k65536), d = gio1<T>::ld(xv + m, k65536);
+    H0[P::phys(0)] = 0.5f * (s + d);
+    H1[P::phys(0)] = 0.5f * (s - d);
+    H0[P::phys(m / 2)] = gio1<T>::ld(xv + m / 2, k65536);
+    H1[P::phys(m / 2)] = -gio1<T>::ld(xv + 3 * m / 2, k65536);
   }
 }
 
