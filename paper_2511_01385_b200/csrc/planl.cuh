@@ -206,11 +206,14 @@ __device__ __forceinline__ void pl_set_in(float (&zr)[M], float (&zi)[M], float*
   }
 }
 
+// skipB0 (forward, H side): leave out the B stores of q = 0 and q = M/2 — pass 2's paired DC sets, whose
+// window-2 store base is shifted by one block (pair_dc_fwd_inplace): q = 0 would leave the window and
+// q = M/2 (slot 32 * 16) would take the pad offset of the block before it; the caller stores those two.
 template <typename P, int M, bool kInv, typename OFF, bool kHalfB = false, bool kG = false,
           typename ST = gio<typename P::elem>>
 __device__ __forceinline__ void pl_set_out(const float (&zr)[M], const float (&zi)[M], float* pa, float* pb,
                                            bool half, typename P::elem* ga = nullptr, typename P::elem* gb = nullptr,
-                                           int m0 = 0) {
+                                           int m0 = 0, bool skipB0 = false) {
   constexpr int LM = ilog2c<M>();
   auto A = [&](auto J) -> float& {
     constexpr int j = decltype(J)::value;
@@ -237,11 +240,11 @@ __device__ __forceinline__ void pl_set_out(const float (&zr)[M], const float (&z
         }
       } else if constexpr (q < M / 2) {  // (half set: B(M-1-q) is another slot of the same set)
         A(Q) = zr[q];
-        B(ct::ic<M - 1 - q>{}) = zi[q];
+        if (q != 0 || !skipB0) B(ct::ic<M - 1 - q>{}) = zi[q];
       } else if constexpr (!kHalfB) {
         if (!half) {
           A(Q) = -zi[q];
-          B(ct::ic<M - 1 - q>{}) = zr[q];
+          if (q != M / 2 || !skipB0) B(ct::ic<M - 1 - q>{}) = zr[q];
         }
       }
     });
@@ -407,6 +410,31 @@ __device__ __forceinline__ void pair_nyq_fwd_out(float (&zr)[M], float (&zi)[M])
     zi[q] = br - ar;  // Im U2_q
     zi[r] = bi - ai;  // -Im U1_q
     zr[r] = ai + bi;  // Re U2_q
+  });
+}
+// Forward pass 2, paired DC sets, in place for the regular store code with window 2's store base one
+// block further (pb = window 2 + 0, so B(M-1-t) = its slot 32 (32 - t)): window 1 slot 32 t <- (t < 16 ?
+// zr[t] : -zi[t]), window 2 slot 32 (32 - t) <- (t < 16 ? zi[t] : zr[t]) for t >= 1; window 2's slot 0
+// (P2[0], left in zi[0]) is stored by the caller.  X1 = Z_q + conj Z_{-q}, X2 = -i (Z_q - conj Z_{-q}):
+// every pair (q, 32 - q) maps onto its own four registers (no permutation: it spilled next to the bf16
+// forward's prefetch registers).
+template <int M>
+__device__ __forceinline__ void pair_dc_fwd_inplace(float (&zr)[M], float (&zi)[M]) {
+  static_assert(M == 32, "pass-2 sets");
+  {
+    const float r0 = zr[0], i0 = zi[0], r16 = zr[16], i16 = zi[16];
+    zr[0] = r0 + r0;      // P1[0]
+    zi[0] = i0 + i0;      // P2[0] (stored by the caller)
+    zr[16] = i16 + i16;   // P2[16]  (window 2 slot 32 * 16 <- zr[16])
+    zi[16] = -(r16 + r16);  // -P1[16] (window 1 slot 32 * 16 <- -zi[16])
+  }
+  ct::static_for<1, 16>([&](auto Q) {
+    constexpr int q = decltype(Q)::value, r = 32 - q;
+    const float a = zr[q], b = zr[r], c = zi[q], d = zi[r];
+    zr[q] = a + b;  // P1[q] = Re X1_q
+    zi[r] = d - c;  // -P1[r], P1[r] = Im X1_q = zi_q - zi_r
+    zi[q] = b - a;  // P2[r] = Im X2_q  (window 2 slot 32 r <- zi[q])
+    zr[r] = c + d;  // P2[q] = Re X2_q  (window 2 slot 32 q <- zr[r])
   });
 }
 // Forward pass 2, paired DC sets: X1 = Z_q + conj Z_{-q}, X2 = -i (Z_q - conj Z_{-q}) stored as the two
@@ -576,10 +604,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   float* H1 = r == 0 ? Hpeer : H;
   constexpr int64_t NV = (int64_t)N * NC;  // elements per vector
   constexpr int XS = NC;                   // element stride of this CTA's half in the row
-  // pass 2 with paired DC / Nyquist sets (PairFix): measured faster for n <= 16384 except the bf16
-  // forward, whose next-vector prefetch registers it would displace (the divergent fix-up spilled next to
-  // them); slower at n = 32768 (one CTA per SM: r02_v21)
-  constexpr bool kPair = (N <= 16384 && (kInv || sizeof(T) == 4));
+  // pass 2 with paired DC / Nyquist sets (PairFix): measured faster for n <= 16384; slower at n = 32768
+  // (one CTA per SM: r02_v21).  The bf16 forward at n = 8192 stays unpaired: next to its prefetch
+  // registers the pairing spills (8 bytes, ptxas) at the 128-register cap of 4 CTAs per SM.
+  constexpr bool kPair = (N <= 16384) && !(N == 8192 && sizeof(T) == 2 && !kInv);
   for (int e = tid; e < P::TW2N; e += NT) {  // LTw2's 17 columns (the paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
@@ -783,11 +811,14 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         if (act2) {
           float zr[32], zi[32];
           pl_set_in<P, 32, false, OffP2<P>>(zr, zi, pa2, pb2, false, tw2, nullptr, nullptr, 0, 0u, pfix);
-          if (pkind == 1) {
-            pair_dc_fwd_store<P>(zr, zi, pa2, pb2 + 32);
-          } else {
-            if (pkind == 2) pair_nyq_fwd_out(zr, zi);
-            pl_set_out<P, 32, false, OffP2<P>>(zr, zi, pa2, pb2, false);
+          if (pkind == 1) pair_dc_fwd_inplace(zr, zi);
+          else if (pkind == 2) pair_nyq_fwd_out(zr, zi);
+          // one store sequence for every lane (the DC pair's window-2 base one block further)
+          pl_set_out<P, 32, false, OffP2<P>>(zr, zi, pa2, pkind == 1 ? pb2 + 32 : pb2, false, nullptr, nullptr, 0,
+                                             pkind == 1);
+          if (pkind == 1) {  // window 2 slots 0 and 32 * 16: P2[0], P2[16]
+            (pb2 + 32)[OffP2<P>::a(0)] = zi[0];
+            (pb2 + 32)[OffP2<P>::a(16)] = zr[16];
           }
         }
       } else {
