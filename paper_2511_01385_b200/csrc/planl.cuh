@@ -348,8 +348,9 @@ struct PairFix {
   __device__ __forceinline__ void operator()(float (&zr)[M], float (&zi)[M]) const {
     constexpr int LM = ilog2c<M>(), H = M / 2;
     if constexpr (!kInv) {
-      zr[0] *= s0;  // (uniform: every lane, s0 = 1 for the regular sets)
-      zi[0] *= s0;
+      const float sc = kind != 0 ? 0.5f : s0;  // (uniform: every lane; regular sets s0 = 1)
+      zr[0] *= sc;
+      zi[0] *= sc;
     } else if (kind == 1) {
       // loaded: R(q) = (P1[q], P2[M-1-q]) for q < M/2, (P2[M-1-q], -P1[q]) for q >= M/2 (P1 / P2 = the
       // two packed real DC spectra); wanted: R(q) = Z_q = X1_q + i X2_q.
@@ -607,7 +608,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   // pass 2 with paired DC / Nyquist sets (PairFix): measured faster for n <= 16384; slower at n = 32768
   // (one CTA per SM: r02_v21).  The bf16 forward at n = 8192 stays unpaired: next to its prefetch
   // registers the pairing spills (8 bytes, ptxas) at the 128-register cap of 4 CTAs per SM.
-  constexpr bool kPair = (N <= 16384 || (!kInv && NC == 1)) && !(N == 8192 && sizeof(T) == 2 && !kInv);
+  constexpr bool kPair = (N <= 16384 || (!kInv && NC == 1));
   for (int e = tid; e < P::TW2N; e += NT) {  // LTw2's 17 columns (the paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
     pb2 = pkind == 1 ? hw2 - 32 : hw2 - 16;  // B(j) = pb[32 (j + 1)]: window 2 slot 32 j (+ 16)
     tw2.h = TW2 + (pkind == 1 ? 16 : 15);
   }
-  const PairFix<32, kInv> pfix{pkind, pkind != 0 ? 0.5f : 1.0f, true};
+  const PairFix<32, kInv> pfix{pkind, 1.0f, true};
   if (kST && tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
           if (pkind == 1) pair_dc_fwd_inplace(zr, zi);
           else if (pkind == 2) pair_nyq_fwd_out(zr, zi);
           // one store sequence for every lane (the DC pair's window-2 base one block further)
-          pl_set_out<P, 32, false, OffP2<P>>(zr, zi, pa2, pkind == 1 ? pb2 + 32 : pb2, false, nullptr, nullptr, 0,
+          pl_set_out<P, 32, false, OffP2<P>>(zr, zi, pa2, pb2 + (pkind == 1 ? 32 : 0), false, nullptr, nullptr, 0,
                                              pkind == 1);
           if (pkind == 1) {  // window 2 slots 0 and 32 * 16: P2[0], P2[16]
             (pb2 + 32)[OffP2<P>::a(0)] = zi[0];
