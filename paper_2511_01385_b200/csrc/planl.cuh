@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   // pass 2 with paired DC / Nyquist sets (PairFix): measured faster for n <= 16384; slower at n = 32768
   // (one CTA per SM: r02_v21).  The bf16 forward at n = 8192 stays unpaired: next to its prefetch
   // registers the pairing spills (8 bytes, ptxas) at the 128-register cap of 4 CTAs per SM.
-  constexpr bool kPair = (N <= 16384 || (!kInv && NC == 1));
+  constexpr bool kPair = (N <= 16384 || !kInv);
   for (int e = tid; e < P::TW2N; e += NT) {  // LTw2's 17 columns (the paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
