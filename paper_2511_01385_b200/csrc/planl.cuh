@@ -605,10 +605,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   float* H1 = r == 0 ? Hpeer : H;
   constexpr int64_t NV = (int64_t)N * NC;  // elements per vector
   constexpr int XS = NC;                   // element stride of this CTA's half in the row
-  // pass 2 with paired DC / Nyquist sets (PairFix): measured faster for n <= 16384; slower at n = 32768
-  // (one CTA per SM: r02_v21).  The bf16 forward at n = 8192 stays unpaired: next to its prefetch
-  // registers the pairing spills (8 bytes, ptxas) at the 128-register cap of 4 CTAs per SM.
-  constexpr bool kPair = (N <= 16384 || !kInv);
+  // pass 2 with paired DC / Nyquist sets (PairFix, pair_dc_fwd_inplace / pair_nyq_fwd_out): faster or
+  // equal in every (n, direction, dtype) cell measured except the one-CTA bf16 n = 32768 inverse
+  // (0.319 -> 0.306 of HBM, r02_v31), which keeps one lane per half-warp on the k = 16 + DC sets.
+  constexpr bool kPair = !(N == 32768 && kInv && sizeof(T) == 2 && NC == 1);
   for (int e = tid; e < P::TW2N; e += NT) {  // LTw2's 17 columns (the paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
