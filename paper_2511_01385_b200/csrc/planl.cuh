@@ -49,7 +49,8 @@ struct PlanL {
   static constexpr int K3PT = K3 / NT;
   static constexpr int MINB = 512 / NT;  // CTAs per SM the 128-register budget allows
   static_assert(S / 2 == NW2 * 16 || NT == 512, "pass-2 sets per thread");
-  static constexpr int TW2N = 32 * 17, TW3N = (M3 / 4) * K3;
+  // TW2: 32 x 17 pass-2 twiddles, then W_32^t (t < 16) for the warp-cooperative pass-3 DC set (dc_warp_dit)
+  static constexpr int TW2N = 32 * 17 + 16, TW3N = (M3 / 4) * K3;
   static constexpr int HPAD = 64;  // additive pad: 4 floats per n/16 slots (see phys)
   static constexpr size_t TW2_OFF = (size_t)(N + HPAD) * 4;
   static constexpr size_t TW3_OFF = TW2_OFF + (size_t)TW2N * 8;
@@ -572,6 +573,29 @@ struct pair_ld<float> {
   __device__ __forceinline__ static uint32_t sel(int r) { return (uint32_t)r; }
 };
 
+// Pass 3's block-DC set (a real M3-point DFT, M3 <= 32) as a warp-cooperative radix-2 DIT over lanes
+// (round 2): lane l holds element l in bit-reversed input order, stage h exchanges with lane l ^ h by
+// shuffles and applies W_{2h}^{l mod h} = W_32^{(l mod h) 32 / 2h} from a 16-entry table; lane q ends with
+// X_q (natural order; inverse: conjugate twiddles, unscaled).  It replaces the real FFT that the thread of
+// the zero-imaginary set ran after that set, which made its warp — at n = 32768, with one set per thread,
+// the whole CTA at the barrier after pass 3 — wait 1.5 sets' time.
+template <int M, bool kInv>
+__device__ __forceinline__ float2 dc_warp_dit(float2 v, int lane, const float2* W32) {
+#pragma unroll
+  for (int h = 1; h < M; h <<= 1) {
+    const float pr = __shfl_xor_sync(0xffffffffu, v.x, h);
+    const float pi = __shfl_xor_sync(0xffffffffu, v.y, h);
+    const bool up = (lane & h) != 0;
+    const float ar = up ? pr : v.x, ai = up ? pi : v.y;  // lower element of the pair
+    const float br = up ? v.x : pr, bi = up ? v.y : pi;  // upper element
+    float2 w = W32[(lane & (h - 1)) * (16 / h)];
+    if (kInv) w.y = -w.y;
+    const float tr = fmaf(br, w.x, -bi * w.y), ti = fmaf(br, w.y, bi * w.x);
+    v = up ? make_float2(ar - tr, ai - ti) : make_float2(ar + tr, ai + ti);
+  }
+  return v;
+}
+
 // NC = 1: one vector of n = N per CTA.  NC = 2: one vector of n = 2N per cluster pair (see header).
 template <typename P, bool kInv, int NC = 1>
 __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem* __restrict__ x, int64_t batch) {
@@ -609,13 +633,19 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   // equal in every (n, direction, dtype) cell measured except the one-CTA bf16 n = 32768 inverse
   // (0.319 -> 0.306 of HBM, r02_v31), which keeps one lane per half-warp on the k = 16 + DC sets.
   constexpr bool kPair = !(N == 32768 && kInv && sizeof(T) == 2 && NC == 1);
-  for (int e = tid; e < P::TW2N; e += NT) {  // LTw2's 17 columns (the paired ones: 1/2 in the forward)
+  for (int e = tid; e < 32 * LTw2::kStride; e += NT) {  // LTw2's 17 columns (paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
     const float h = (!kInv && kPair && col >= 15) ? 0.5f : 1.0f;
     float s, c;
     sincospif(2.0f * (float)(k * rev_bits<5>(j)) / 1024.0f, &s, &c);
     TW2[e] = make_float2(h * c, h * sg * s);
+  }
+  const float2* W32 = TW2 + 32 * LTw2::kStride;  // W_32^t, t < 16 (forward sign; dc_warp_dit conjugates)
+  for (int t = tid; t < 16; t += NT) {
+    float s, c;
+    sincospif((float)t / 16.0f, &s, &c);
+    TW2[32 * LTw2::kStride + t] = make_float2(c, -s);
   }
   for (int e = tid; e < P::TW3N; e += NT) {
     const int a = e / K3, k = 1 + e % K3;
@@ -645,6 +675,51 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   const uint32_t k65536 = kTwo16;
   T* SR = reinterpret_cast<T*>(H);  // kST: the staged natural-order row (aliases H)
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + P::BAR_OFF);
+  // pass 3's DC set: the last warp, cooperatively (dc_warp_dit).  Its natural-order side is the global row
+  // (one-CTA plan), the staged row SR (kST) or H (cluster pair); its H side is slots OffP3::a(j).
+  // (kDCW off: the bf16 n = 8192 forward, whose staged pass 3 spills with the warp's two extra registers
+  // next to its prefetch and pass-2 pairs; there the zero-imaginary set's thread runs the DC set too)
+  constexpr bool kDCW = !(N == 8192 && sizeof(T) == 2 && !kInv && kST);
+  constexpr int LM3 = ilog2c<M3>();
+  const bool dcw = kDCW && tid >= NT - 32;
+  const int dl = tid & 31;
+  auto dc_row_ld = [&](const T* row, int s_) -> float {
+    if constexpr (NC == 2) return H[OffP3<P>::a(s_)];
+    else if constexpr (kST) return sio1<T>::ld(SR + 1024 * s_, k65536);
+    else return gio1<T>::ld(row + 1024 * s_, k65536);
+  };
+  auto dc_row_st = [&](T* row, int s_, float val) {
+    if constexpr (NC == 2) H[OffP3<P>::a(s_)] = val;
+    else if constexpr (kST) sst1<T>::st1(SR + 1024 * s_, val);
+    else gio<T>::st1(row + 1024 * s_, val);
+  };
+  auto dc_in = [&](auto inv, const T* row) -> float2 {  // (the whole DC warp)
+    constexpr bool kI = decltype(inv)::value;
+    float2 v = make_float2(0.f, 0.f);
+    if (dl < M3) {
+      if constexpr (!kI) {
+        v.x = H[OffP3<P>::a(dl)];  // element dl in bit-reversed order (the per-stage invariant)
+      } else {  // X_q, q = rev(dl), from the packed spectrum (X_{M-q} = conj X_q)
+        const int q = (int)(__brev((unsigned)dl) >> (32 - LM3));
+        const int qa = q <= M3 / 2 ? q : M3 - q;
+        const float re = dc_row_ld(row, qa);
+        const float im = (qa == 0 || qa == M3 / 2) ? 0.f : dc_row_ld(row, M3 - qa);
+        v = make_float2(re, q <= M3 / 2 ? im : -im);
+      }
+    }
+    return dc_warp_dit<M3, kI>(v, dl, W32);
+  };
+  auto dc_out = [&](auto inv, T* row, float2 v) {
+    constexpr bool kI = decltype(inv)::value;
+    if (dl < M3) {
+      if constexpr (!kI) {  // packed: slot 1024 q <- Re X_q (q <= M/2), slot 1024 (M - q) <- Im X_q
+        if (dl <= M3 / 2) dc_row_st(row, dl, v.x);
+        if (dl >= 1 && dl < M3 / 2) dc_row_st(row, M3 - dl, v.y);
+      } else {  // x_t (times M, unscaled) -> H slot rev(t), scaled by 1/N
+        H[OffP3<P>::a((int)(__brev((unsigned)dl) >> (32 - LM3)))] = v.x * (1.0f / N);
+      }
+    }
+  };
   auto pass3 = [&](auto inv, T* xv) {
     constexpr bool kI = decltype(inv)::value;
     if constexpr (kST) {
@@ -659,37 +734,47 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       ct::static_for<0, KP>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int kk = tid + NT * i;
-        if (i == 0 && kk == 0) {
-          float d[M3];
+        if (i == 0 && kk == 0) {  // the zero-imaginary set (the DC set: the last warp, below)
           pl_set_in<P, M3, kI, OffP3<P>, true, true, SIO>(zr[i], zi[i], H + K3, H - K3, true, tw3_for(K3), SR + K3,
                                                           SR - K3, 1024, k65536);
-          pl_dc_g_in<P, M3, kI, OffP3<P>, SIO>(d, H, SR, 1024, k65536);
-          ct::static_for<0, M3>([&](auto J) {
-            constexpr int j = decltype(J)::value;
-            if constexpr (kI) zi[i][j] = d[j];
-            else if constexpr (j < M3 / 2) zr[i][M3 / 2 + j] = d[j];
-            else zi[i][j] = d[j];
-          });
+          if constexpr (!kDCW) {  // ... or this thread: its DC results in the registers the half set leaves free
+            float d[M3];
+            pl_dc_g_in<P, M3, kI, OffP3<P>, SIO>(d, H, SR, 1024, k65536);
+            ct::static_for<0, M3>([&](auto J) {
+              constexpr int j = decltype(J)::value;
+              if constexpr (kI) zi[i][j] = d[j];
+              else if constexpr (j < M3 / 2) zr[i][M3 / 2 + j] = d[j];
+              else zi[i][j] = d[j];
+            });
+          }
         } else {
           pl_set_in<P, M3, kI, OffP3<P>, false, true, SIO>(zr[i], zi[i], H + kk, H - kk, false, tw3_for(kk),
                                                            SR + kk, SR - kk, 1024, k65536);
         }
       });
+      float2 dcv = make_float2(0.f, 0.f);
+      if (dcw) dcv = dc_in(inv, xv);
       __syncthreads();  // every set read: H / SR free for the writes
+      if (dcw) dc_out(inv, xv, dcv);
       ct::static_for<0, KP>([&](auto I) {
         constexpr int i = decltype(I)::value;
         const int kk = tid + NT * i;
         if (i == 0 && kk == 0) {
-          float d[M3];
-          ct::static_for<0, M3>([&](auto J) {
-            constexpr int j = decltype(J)::value;
-            if constexpr (kI) d[j] = zi[i][j];
-            else if constexpr (j < M3 / 2) d[j] = zr[i][M3 / 2 + j];
-            else d[j] = zi[i][j];
-          });
-          pl_set_out<P, M3, kI, OffP3<P>, true, true, SST>(zr[i], zi[i], H + K3, H - K3, true, SR + K3, SR - K3,
-                                                           1024);
-          pl_dc_g_out<P, M3, kI, OffP3<P>, SST>(d, H, SR, 1024, kI ? 1.0f / N : 1.0f);
+          if constexpr (!kDCW) {
+            float d[M3];
+            ct::static_for<0, M3>([&](auto J) {
+              constexpr int j = decltype(J)::value;
+              if constexpr (kI) d[j] = zi[i][j];
+              else if constexpr (j < M3 / 2) d[j] = zr[i][M3 / 2 + j];
+              else d[j] = zi[i][j];
+            });
+            pl_set_out<P, M3, kI, OffP3<P>, true, true, SST>(zr[i], zi[i], H + K3, H - K3, true, SR + K3, SR - K3,
+                                                             1024);
+            pl_dc_g_out<P, M3, kI, OffP3<P>, SST>(d, H, SR, 1024, kI ? 1.0f / N : 1.0f);
+          } else {
+            pl_set_out<P, M3, kI, OffP3<P>, true, true, SST>(zr[i], zi[i], H + K3, H - K3, true, SR + K3, SR - K3,
+                                                             1024);
+          }
         } else {
           pl_set_out<P, M3, kI, OffP3<P>, false, true, SST>(zr[i], zi[i], H + kk, H - kk, false, SR + kk, SR - kk,
                                                             1024);
@@ -700,17 +785,14 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
 #pragma unroll 1
     for (int i = 0; i < P::K3PT; ++i) {
       const int kk = tid + NT * i;
-      if (kk == 0) {  // the zero-imaginary set k = 512 and the DC set
+      if (kk == 0) {  // the zero-imaginary set k = 512 (the DC set: the last warp, below)
         pl_set<P, M3, kI, OffP3<P>, true, kG3>(H + K3, H - K3, true, tw3_for(K3), xv + K3, xv - K3, 1024, k65536);
-        if constexpr (kG3)
-          pl_dc_g<P, M3, kI, OffP3<P>>(H, xv, 1024, kI ? 1.0f / N : 1.0f, k65536);
-        else
-          pl_dc<P, M3, kI, OffP3<P>>(H, kI ? 1.0f / N : 1.0f);
       } else {
         pl_set<P, M3, kI, OffP3<P>, false, kG3>(H + kk, H - kk, false, tw3_for(kk), xv + kk, xv - kk, 1024,
                                                 k65536);
       }
     }
+    if (dcw) dc_out(inv, xv, dc_in(inv, xv));  // (every lane loads before any lane stores: in place is safe)
   };
   // pass-2 lane: window ww, k2 = 1 .. 15; lane 0 of each window: k2 = 16 (zero imaginary) + DC
   // The two half-warps take blocks ww and ww + D, D = n/4096: their pads then differ by 16 floats
