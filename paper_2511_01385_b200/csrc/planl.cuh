@@ -596,6 +596,17 @@ __device__ __forceinline__ float2 dc_warp_dit(float2 v, int lane, const float2* 
   return v;
 }
 
+// Split cluster barrier (the pair's write-after-read hand-off): arrive after this CTA's last read of the
+// peer's / its own H, wait just before the next write into H, so the barrier latency overlaps the work in
+// between (the next pass 1's loads and register FFT; the inverse pass 1's FFT and stores) instead of a
+// full cluster.sync() at the end of every vector.
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // NC = 1: one vector of n = N per CTA.  NC = 2: one vector of n = 2N per cluster pair (see header).
 template <typename P, bool kInv, int NC = 1>
 __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem* __restrict__ x, int64_t batch) {
@@ -876,6 +887,9 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
           }
         }
         rfft_fwd_reg<R>(b);
+        if constexpr (NC == 2) {  // the peer has finished the previous vector's cross stage (reads of this H)
+          if (it > 0) cluster_wait_acquire();
+        }
         if constexpr (kST) {  // the previous vector's bulk store still reads SR (= H)
           if (tid == 0) bulk_wait_read<0>();
           __syncthreads();  // (kST: S / 2 == NT, every thread is here)
@@ -925,10 +939,11 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       } else {
         cooperative_groups::this_cluster().sync();  // both windows complete and visible
         pl_cross_fwd<P>(H0, H1, TWCa, twb, xv, r, tid);
-        cooperative_groups::this_cluster().sync();  // the peer is done reading this H
+        cluster_arrive_release();  // this CTA is done reading both H; the wait sits before the next H write
       }
     } else {
       if constexpr (NC == 2) {
+        if (it > 0) cluster_wait_acquire();  // the peer has read its H (the previous vector's pass 1)
         pl_cross_inv<P>(H0, H1, TWCa, twb, xv, r, tid, k65536);
         cooperative_groups::this_cluster().sync();  // both windows written (half of each remotely)
       }
@@ -965,6 +980,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
           __syncthreads();
           if (tid == 0 && v + gridDim.x < batch) issue_row(v + gridDim.x);
         }
+        if constexpr (NC == 2) cluster_arrive_release();  // H read; the wait sits before the next cross stage
         rfft_inv_reg<R>(b);
         ct::static_for<0, R>([&](auto I) {
           constexpr int i = decltype(I)::value;
@@ -981,10 +997,11 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         // after its own barrier
       } else if constexpr (NC == 1) {
         __syncthreads();
-      } else {
-        cooperative_groups::this_cluster().sync();  // the peer's next cross stage writes this H
       }
     }
+  }
+  if constexpr (NC == 2) {  // match the last arrive: the peer may still read this CTA's H
+    if (it > 0) cluster_wait_acquire();
   }
   if constexpr (kST && !kInv) {
     if (tid == 0) bulk_wait<0>();
