@@ -295,13 +295,6 @@ __device__ __forceinline__ void pl_dc_g_out(const float (&d)[M], float* p0, type
       p0[OFF::a(j)] = d[j] * scale;
   });
 }
-template <typename P, int M, bool kInv, typename OFF>
-__device__ __forceinline__ void pl_dc_g(float* p0, typename P::elem* g0, int m0, float scale, uint32_t k65536) {
-  float d[M];
-  pl_dc_g_in<P, M, kInv, OFF>(d, p0, g0, m0, k65536);
-  pl_dc_g_out<P, M, kInv, OFF>(d, p0, g0, m0, scale);
-}
-
 // DC set: slots p0[OFF::a(j)] (j < M) — the packed real M-point FFT (inverse: unscaled x scale).
 template <typename P, int M, bool kInv, typename OFF>
 __device__ __forceinline__ void pl_dc(float* p0, float scale) {
@@ -439,27 +432,6 @@ __device__ __forceinline__ void pair_dc_fwd_inplace(float (&zr)[M], float (&zi)[
     zr[r] = c + d;  // P2[q] = Re X2_q  (window 2 slot 32 q <- zr[r])
   });
 }
-// Forward pass 2, paired DC sets: X1 = Z_q + conj Z_{-q}, X2 = -i (Z_q - conj Z_{-q}) stored as the two
-// windows' packed real 32-point spectra (slot 32 s of window w at hw + OffP2::a(s)); its own stores (the
-// regular store order would need a register permutation, which spilled next to the bf16 prefetch).
-template <typename P, int M>
-__device__ __forceinline__ void pair_dc_fwd_store(const float (&zr)[M], const float (&zi)[M], float* hw1,
-                                                  float* hw2) {
-  static_assert(M == 32, "pass-2 sets");
-  using OFF = OffP2<P>;
-  hw1[OFF::a(0)] = zr[0] + zr[0];
-  hw2[OFF::a(0)] = zi[0] + zi[0];
-  hw1[OFF::a(16)] = zr[16] + zr[16];
-  hw2[OFF::a(16)] = zi[16] + zi[16];
-  ct::static_for<1, 16>([&](auto Q) {
-    constexpr int q = decltype(Q)::value, r = 32 - q;
-    hw1[OFF::a(q)] = zr[q] + zr[r];  // Re X1_q
-    hw1[OFF::a(r)] = zi[q] - zi[r];  // Im X1_q
-    hw2[OFF::a(q)] = zi[q] + zi[r];  // Re X2_q
-    hw2[OFF::a(r)] = zr[r] - zr[q];  // Im X2_q
-  });
-}
-
 // Cluster-pair cross stage (m = N, the vector has 2N slots), forward: groups k in this CTA's
 // quarter, A from window 0 (H0), B from window 1 (H1), outputs straight to the global row xv.
 // U groups per batch: all their shared (local and peer) loads first, then the arithmetic and the
