@@ -613,9 +613,9 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   constexpr int64_t NV = (int64_t)N * NC;  // elements per vector
   constexpr int XS = NC;                   // element stride of this CTA's half in the row
   // pass 2 with paired DC / Nyquist sets (PairFix, pair_dc_fwd_inplace / pair_nyq_fwd_out): faster or
-  // equal in every (n, direction, dtype) cell measured except the one-CTA bf16 n = 32768 inverse
-  // (0.319 -> 0.306 of HBM, r02_v31), which keeps one lane per half-warp on the k = 16 + DC sets.
-  constexpr bool kPair = !(N == 32768 && kInv && sizeof(T) == 2 && NC == 1);
+  // equal in every (n, direction, dtype) cell measured (the bf16 n = 32768 inverse, slower before pass 3's
+  // DC set moved to a warp of its own, 0.319 -> 0.306 in r02_v31, gains since: 0.320 -> 0.333, r02_v41)
+  constexpr bool kPair = true;
   for (int e = tid; e < 32 * LTw2::kStride; e += NT) {  // LTw2's 17 columns (paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
