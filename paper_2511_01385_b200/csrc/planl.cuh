@@ -295,24 +295,6 @@ __device__ __forceinline__ void pl_dc_g_out(const float (&d)[M], float* p0, type
       p0[OFF::a(j)] = d[j] * scale;
   });
 }
-// DC set: slots p0[OFF::a(j)] (j < M) — the packed real M-point FFT (inverse: unscaled x scale).
-template <typename P, int M, bool kInv, typename OFF>
-__device__ __forceinline__ void pl_dc(float* p0, float scale) {
-  float d[M];
-  ct::static_for<0, M>([&](auto J) {
-    constexpr int j = decltype(J)::value;
-    d[j] = p0[OFF::a(j)];
-  });
-  if (!kInv)
-    rfft_fwd_reg<M>(d);
-  else
-    rfft_inv_reg<M>(d);
-  ct::static_for<0, M>([&](auto J) {
-    constexpr int j = decltype(J)::value;
-    p0[OFF::a(j)] = d[j] * scale;
-  });
-}
-
 // pass-2 twiddle: TW2[j][c] (17 columns), indexed by natural j: c = k - 1 (k = 1 .. 15) W_1024^{k rev5(j)};
 // c = 15 the paired block-Nyquist sets (k = 16), c = 16 the paired block-DC sets (k = 0, no twiddle).
 // Forward: the paired columns carry the factor 1/2 of the two-for-one split (PairFix); inverse: conj.
@@ -612,14 +594,13 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
   float* H1 = r == 0 ? Hpeer : H;
   constexpr int64_t NV = (int64_t)N * NC;  // elements per vector
   constexpr int XS = NC;                   // element stride of this CTA's half in the row
-  // pass 2 with paired DC / Nyquist sets (PairFix, pair_dc_fwd_inplace / pair_nyq_fwd_out): faster or
-  // equal in every (n, direction, dtype) cell measured (the bf16 n = 32768 inverse, slower before pass 3's
-  // DC set moved to a warp of its own, 0.319 -> 0.306 in r02_v31, gains since: 0.320 -> 0.333, r02_v41)
-  constexpr bool kPair = true;
+  // pass 2 runs paired DC / Nyquist sets (PairFix, pair_dc_fwd_inplace / pair_nyq_fwd_out) in every
+  // (n, direction, dtype) cell: faster or equal everywhere once pass 3's DC set moved to a warp of its own
+  // (the bf16 n = 32768 inverse 0.320 -> 0.333 of HBM, r02_v41; before that it had measured slower, r02_v31)
   for (int e = tid; e < 32 * LTw2::kStride; e += NT) {  // LTw2's 17 columns (paired ones: 1/2 in the forward)
     const int j = e / LTw2::kStride, col = e % LTw2::kStride;
     const int k = col == 16 ? 0 : col + 1;
-    const float h = (!kInv && kPair && col >= 15) ? 0.5f : 1.0f;
+    const float h = (!kInv && col >= 15) ? 0.5f : 1.0f;
     float s, c;
     sincospif(2.0f * (float)(k * rev_bits<5>(j)) / 1024.0f, &s, &c);
     TW2[e] = make_float2(h * c, h * sg * s);
@@ -777,21 +758,20 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
     }
     if (dcw) dc_out(inv, xv, dc_in(inv, xv));  // (every lane loads before any lane stores: in place is safe)
   };
-  // pass-2 lane: window ww, k2 = 1 .. 15; lane 0 of each window: k2 = 16 (zero imaginary) + DC
+  // pass-2 lane: window ww, k2 = 1 .. 15; lane 0 of each half-warp: a paired DC or Nyquist set (below)
   // The two half-warps take blocks ww and ww + D, D = n/4096: their pads then differ by 16 floats
   // (4 pad periods), so the half-warps' scalar accesses fall on complementary bank halves (with
   // adjacent blocks they overlapped: 2-way conflicts on every pass-2 access).
   constexpr int D2 = N / 4096;
   const int w32 = tid / 32, hw = (tid / 16) & 1;
-  const int ww = (w32 % D2) + (w32 / D2) * 2 * D2 + hw * D2, k2 = (kPair || tid % 16 != 0) ? tid % 16 : 16;
+  const int ww = (w32 % D2) + (w32 / D2) * 2 * D2 + hw * D2, k2 = tid % 16;
   const bool act2 = tid < P::NW2 * 16;
   float* h2 = H + P::phys(ww * 1024);  // block base (pad of the block start; OffP2 adds the rest)
   // lanes k2 = 1 .. 15: set k2 of window ww; lane k2 = 0 of each half-warp: a paired set (PairFix) of the
   // warp's two windows w1 = ww(hw 0), w2 = w1 + D2 — block DCs on half-warp 0, block Nyquists on half-warp
   // 1.  Their slots 32 j (+ 16) then fall on the two banks the 30 regular lanes leave free (the half-warps'
   // pads differ by 16 floats): a pairing across other windows put a 2-way conflict on every pass-2 access.
-  // (!kPair: lane 0 of a half-warp runs its window's k = 16 set with a zero imaginary part, then its DC set)
-  const int pkind = (!kPair || k2 != 0) ? 0 : (hw == 0 ? 1 : 2);
+  const int pkind = k2 != 0 ? 0 : (hw == 0 ? 1 : 2);
   float* pa2 = h2 + k2;
   float* pb2 = h2 - k2;
   LTw2 tw2;
@@ -876,7 +856,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
         });
       }
       __syncthreads();
-      if constexpr (kPair) {
+      {
         if (act2) {
           float zr[32], zi[32];
           pl_set_in<P, 32, false, OffP2<P>>(zr, zi, pa2, pb2, false, tw2, nullptr, nullptr, 0, 0u, pfix);
@@ -890,9 +870,6 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
             (pb2 + 32)[OffP2<P>::a(16)] = zr[16];
           }
         }
-      } else {
-        if (act2) pl_set<P, 32, false, OffP2<P>>(pa2, pb2, k2 == 16, tw2);
-        if (act2 && k2 == 16) pl_dc<P, 32, false, OffP2<P>>(h2, 1.0f);
       }
       __syncthreads();
       pass3(std::false_type{}, xv);
@@ -922,15 +899,10 @@ __global__ void __launch_bounds__(P::NT, P::MINB) rdfftl_kernel(typename P::elem
       if constexpr (kST) mbar_wait(bar, it & 1);  // this vector's row staged in SR
       pass3(std::true_type{}, xv);  // NC = 1: reads the row straight from HBM (kST: from SR)
       __syncthreads();
-      if constexpr (kPair) {
-        if (act2) {
-          float zr[32], zi[32];
-          pl_set_in<P, 32, true, OffP2<P>>(zr, zi, pa2, pb2, false, tw2, nullptr, nullptr, 0, 0u, pfix);
-          pl_set_out<P, 32, true, OffP2<P>>(zr, zi, pa2, pb2, false);
-        }
-      } else {
-        if (act2) pl_set<P, 32, true, OffP2<P>>(pa2, pb2, k2 == 16, tw2);
-        if (act2 && k2 == 16) pl_dc<P, 32, true, OffP2<P>>(h2, 1.0f);
+      if (act2) {
+        float zr[32], zi[32];
+        pl_set_in<P, 32, true, OffP2<P>>(zr, zi, pa2, pb2, false, tw2, nullptr, nullptr, 0, 0u, pfix);
+        pl_set_out<P, 32, true, OffP2<P>>(zr, zi, pa2, pb2, false);
       }
       __syncthreads();
       if (tid < S / 2) {  // inverse pass 1
